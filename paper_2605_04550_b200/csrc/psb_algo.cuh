@@ -1,0 +1,552 @@
+// psb_algo.cuh — per-point arithmetic of the sigma_min(zI - A) evaluator (K1).
+//
+// Replaces the per-z dense SVD of the reference
+//   pseudospec/core.py:141-168  smin_many   (np.linalg.svd(zI - A)[-1], LAPACK zgesdd)
+// by two exact-arithmetic engines that only touch the band of A:
+//
+//   engine L ("Lanczos"): pivoted band LU of M = zI - A (gbtrf-style, pivots within
+//     the band, fill up to kl+ku superdiagonals), then inverse Lanczos on
+//     (M^H M)^{-1} = M^{-1} M^{-H} (four banded triangular sweeps per step) with
+//     the 3-term recurrence; sigma = 1/sqrt(theta_max). Used where sigma_min is
+//     small relative to ||M|| (isolated, fast convergence: 2-12 steps measured).
+//
+//   engine B ("bisection"): sigma_min^2 is the smallest lambda at which
+//     G(lambda) = A^H A - conj(z) A - z A^H + (|z|^2 - lambda) I   (= M^H M - lambda I)
+//     stops being positive definite. A pivot-free banded LDL^H (stable on the PD
+//     side, where every accepted test lives) decides each bisection step. All
+//     z-independent bands are shared, so the state is a b x b register window
+//     (b = kl+ku) and the engine is FP64-bound. Used where sigma_min >= tau*S,
+//     S = |z| + ||A||_2 bound; there the rounding of G (~eps*S^2) costs at most
+//     eps/tau^2 relative accuracy, and Toeplitz-like continua of singular values
+//     (which stall Lanczos) do not slow bisection.
+//
+// Every function here is __host__ __device__ so the identical arithmetic can be
+// exercised on the host by tools/algo_mirror.cu (a test tool, never a product path).
+#pragma once
+#include <stdint.h>
+#include <math.h>
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#define PSB_HD __host__ __device__ __forceinline__
+#else
+#error "compile with nvcc"
+#endif
+
+namespace psb {
+
+// ---------------------------------------------------------------- complex helpers
+PSB_HD double2 cmk(double a, double b) { double2 r; r.x = a; r.y = b; return r; }
+PSB_HD double2 czero() { return cmk(0.0, 0.0); }
+PSB_HD double2 cconj(double2 a) { return cmk(a.x, -a.y); }
+PSB_HD double2 cadd(double2 a, double2 b) { return cmk(a.x + b.x, a.y + b.y); }
+PSB_HD double2 csub(double2 a, double2 b) { return cmk(a.x - b.x, a.y - b.y); }
+PSB_HD double2 cscale(double2 a, double s) { return cmk(a.x * s, a.y * s); }
+PSB_HD double2 cmul(double2 a, double2 b) {
+  return cmk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a - b*c   (the chained operand c enters last: depth 2 from c)
+PSB_HD double2 cfms(double2 a, double2 b, double2 c) {
+  return cmk(fma(-b.x, c.x, fma(b.y, c.y, a.x)), fma(-b.x, c.y, fma(-b.y, c.x, a.y)));
+}
+// a - conj(b)*c
+PSB_HD double2 cfms_cj(double2 a, double2 b, double2 c) {
+  return cmk(fma(-b.x, c.x, fma(-b.y, c.y, a.x)), fma(-b.x, c.y, fma(b.y, c.x, a.y)));
+}
+// a - s*c with real s
+PSB_HD double2 cfms_r(double2 a, double s, double2 c) { return cmk(fma(-s, c.x, a.x), fma(-s, c.y, a.y)); }
+PSB_HD double cnorm2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+PSB_HD double cabs1(double2 a) { return fabs(a.x) + fabs(a.y); }
+// Re(conj(a) * b)
+PSB_HD double cdotr(double2 a, double2 b) { return fma(a.x, b.x, a.y * b.y); }
+// 1/d, scaled (Smith) so |d| near the overflow/underflow range stays finite
+PSB_HD double2 crcp(double2 d) {
+  if (fabs(d.x) >= fabs(d.y)) {
+    double r = d.y / d.x, den = fma(d.y, r, d.x);
+    double inv = 1.0 / den;
+    return cmk(inv, -r * inv);
+  } else {
+    double r = d.x / d.y, den = fma(d.x, r, d.y);
+    double inv = 1.0 / den;
+    return cmk(r * inv, -inv);
+  }
+}
+
+// Lane view of a lane-interleaved array: element i lives at p[i * ld].
+struct LV {
+  double2* p;
+  int ld;
+  PSB_HD double2 get(int64_t i) const { return p[i * ld]; }
+  PSB_HD void put(int64_t i, double2 v) const { p[i * ld] = v; }
+};
+struct LVb {
+  uint8_t* p;
+  int ld;
+  PSB_HD int get(int64_t i) const { return p[i * ld]; }
+  PSB_HD void put(int64_t i, int v) const { p[i * ld] = (uint8_t)v; }
+};
+
+// Shape of the band problem. Band of A: Ab[(d + kl) * n + i] = A[i, i + d], d in [-kl, ku].
+// Factor row j (NF = W + 1 + kl complex): [U'(j, j+1..j+W) | rinv_j | L(j, 1..kl)],
+// U' = rinv * U (row-scaled upper factor), W = kl + ku.
+struct Shape {
+  int n, kl, ku, W, NF;
+};
+PSB_HD Shape make_shape(int n, int kl, int ku) {
+  Shape s; s.n = n; s.kl = kl; s.ku = ku; s.W = kl + ku; s.NF = kl + ku + 1 + kl; return s;
+}
+
+// ------------------------------------------------------------ engine L: band LU
+// Pivoted LU of M = zI - A in a sliding register window of (kl+1) rows x (W+1)
+// columns. Pivot rule: first max of |re|+|im| (LAPACK izamax/dcabs1 convention,
+// as zgbtrf). Returns false on an exactly zero pivot (M singular in floating point).
+template <int KLM, int KUM, bool DYN>
+PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z, LV F, LVb piv) {
+  constexpr int WM = KLM + KUM;
+  const int n = s.n;
+  const int kl = DYN ? s.kl : KLM;
+  const int ku = DYN ? s.ku : KUM;
+  const int W = kl + ku;
+  const int NF = W + 1 + kl;
+  double2 win[KLM + 1][WM + 1];
+  bool ok = true;
+  // initial rows r = 0..kl hold matrix rows r, columns 0..W
+#pragma unroll
+  for (int r = 0; r <= KLM; r++) {
+#pragma unroll
+    for (int c = 0; c <= WM; c++) {
+      double2 v = czero();
+      if (r <= kl && c <= W && r < n && c < n) {
+        int d = c - r;
+        if (d >= -kl && d <= ku) {
+          double2 a = Ab[(int64_t)(d + kl) * n + r];
+          v = cmk((d == 0 ? z.x : 0.0) - a.x, (d == 0 ? z.y : 0.0) - a.y);
+        }
+      }
+      win[r][c] = v;
+    }
+  }
+  for (int j = 0; j < n; j++) {
+    // pivot among rows j..j+kl (rows past n are zero and never win a strict '>')
+    int p = 0;
+    double best = cabs1(win[0][0]);
+#pragma unroll
+    for (int r = 1; r <= KLM; r++) {
+      if (r <= kl) {
+        double m = cabs1(win[r][0]);
+        if (m > best) { best = m; p = r; }
+      }
+    }
+#pragma unroll
+    for (int r = 1; r <= KLM; r++) {
+      if (r <= kl && p == r) {
+#pragma unroll
+        for (int c = 0; c <= WM; c++) {
+          double2 t = win[0][c]; win[0][c] = win[r][c]; win[r][c] = t;
+        }
+      }
+    }
+    piv.put(j, p);
+    double2 d = win[0][0];
+    double2 ri;
+    if (d.x == 0.0 && d.y == 0.0) { ok = false; ri = czero(); }
+    else ri = crcp(d);
+    const int64_t rb = (int64_t)j * NF;
+#pragma unroll
+    for (int c = 1; c <= WM; c++)
+      if (c <= W) F.put(rb + c - 1, cmul(win[0][c], ri));
+    F.put(rb + W, ri);
+#pragma unroll
+    for (int r = 1; r <= KLM; r++) {
+      if (r <= kl) {
+        double2 l = cmul(win[r][0], ri);
+        F.put(rb + W + r, l);
+#pragma unroll
+        for (int c = 1; c <= WM; c++)
+          if (c <= W) win[r][c] = cfms(win[r][c], l, win[0][c]);
+      }
+    }
+    // slide the window: row r <- row r+1 shifted one column left
+#pragma unroll
+    for (int r = 0; r < KLM; r++) {
+      if (r < kl) {
+#pragma unroll
+        for (int c = 0; c < WM; c++)
+          if (c < W) win[r][c] = win[r + 1][c + 1];
+        win[r][W < WM ? W : WM] = czero();
+      }
+    }
+    // new bottom row: matrix row i = j+1+kl, columns j+1 .. j+1+W (d = c - kl)
+    const int i = j + 1 + kl;
+#pragma unroll
+    for (int c = 0; c <= WM; c++) {
+      if (c <= W) {
+        double2 v = czero();
+        int col = j + 1 + c;
+        if (i < n && col < n) {
+          double2 a = Ab[(int64_t)c * n + i];
+          v = cmk((c == kl ? z.x : 0.0) - a.x, (c == kl ? z.y : 0.0) - a.y);
+        }
+        win[kl][c] = v;
+      }
+    }
+  }
+  return ok;
+}
+
+// S1: forward sweep, t = U^{-H} r where r is the new Lanczos residual
+//   r_k = w_{k-1} - c1 * RA - c2 * RB   (k >= 2), or the start vector v1 (k == 1).
+// Writes RA <- r_k, RB <- old RA (fixed roles; no per-lane ping-pong), T <- U^{-H} r_k.
+// U^H = U'^H D^H: solve with the unit lower U'^H, then scale by conj(rinv).
+// Returns ||r_k||^2 (k >= 2).
+template <int KLM, int KUM, bool DYN>
+PSB_HD double sweep_s1(const Shape& s, LV F, LV T, LV RA, LV RB, const double2* __restrict__ v1,
+                       int k, double c1, double c2) {
+  constexpr int WM = KLM + KUM;
+  const int n = s.n;
+  const int kl = DYN ? s.kl : KLM;
+  const int W = DYN ? s.W : WM;
+  const int NF = W + 1 + kl;
+  double2 tw[WM + 1];  // tw[d] = t'_{j-d}
+#pragma unroll
+  for (int d = 0; d <= WM; d++) tw[d] = czero();
+  double bsq = 0.0;
+  for (int j = 0; j < n; j++) {
+    double2 r;
+    if (k == 1) {
+      r = v1[j];
+      RA.put(j, r);
+    } else {
+      double2 t = T.get(j), ra = RA.get(j);
+      r = cfms_r(t, c1, ra);
+      if (k >= 3) r = cfms_r(r, c2, RB.get(j));
+      RB.put(j, ra);
+      RA.put(j, r);
+      bsq += cnorm2(r);
+    }
+    double2 tp = r;
+#pragma unroll
+    for (int d = WM; d >= 1; d--) {
+      if (d <= W && j - d >= 0) tp = cfms_cj(tp, F.get((int64_t)(j - d) * NF + d - 1), tw[d]);
+    }
+    double2 ri = F.get((int64_t)j * NF + W);
+    T.put(j, cmul(tp, cconj(ri)));
+#pragma unroll
+    for (int d = WM; d >= 2; d--) tw[d] = tw[d - 1];
+    tw[1] = tp;
+  }
+  return bsq;
+}
+
+// S2: backward sweep, apply E^H (row swaps + unit-lower multipliers, transposed).
+// Returns ||output||^2.
+template <int KLM, int KUM, bool DYN>
+PSB_HD double sweep_s2(const Shape& s, LV F, LVb piv, LV T) {
+  const int n = s.n;
+  const int kl = DYN ? s.kl : KLM;
+  const int W = DYN ? s.W : KLM + KUM;
+  const int NF = W + 1 + kl;
+  double2 yw[KLM + 1];  // yw[r] = y_{j+r}
+#pragma unroll
+  for (int r = 0; r <= KLM; r++) yw[r] = czero();
+  double nrm = 0.0;
+  for (int j = n - 1; j >= 0; j--) {
+    const int out = j + 1 + kl;
+    if (out < n) { T.put(out, yw[kl]); nrm += cnorm2(yw[kl]); }
+#pragma unroll
+    for (int r = KLM; r >= 1; r--) if (r <= kl) yw[r] = yw[r - 1];
+    double2 y = T.get(j);
+    const int64_t rb = (int64_t)j * NF + W;
+#pragma unroll
+    for (int r = KLM; r >= 1; r--)
+      if (r <= kl) y = cfms_cj(y, F.get(rb + r), yw[r]);
+    yw[0] = y;
+    const int p = piv.get(j);
+#pragma unroll
+    for (int r = 1; r <= KLM; r++) {
+      if (r <= kl && p == r) { double2 t = yw[0]; yw[0] = yw[r]; yw[r] = t; }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r <= KLM; r++)
+    if (r <= kl && r < n) { T.put(r, yw[r]); nrm += cnorm2(yw[r]); }
+  return nrm;
+}
+
+// S3: forward sweep, apply E (row swaps + eliminations) to scale * T, in place.
+template <int KLM, int KUM, bool DYN>
+PSB_HD void sweep_s3(const Shape& s, LV F, LVb piv, LV T, double scale) {
+  const int n = s.n;
+  const int kl = DYN ? s.kl : KLM;
+  const int W = DYN ? s.W : KLM + KUM;
+  const int NF = W + 1 + kl;
+  double2 bw[KLM + 1];  // bw[r] = b_{j+r}
+#pragma unroll
+  for (int r = 0; r <= KLM; r++) bw[r] = (r <= kl && r < n) ? cscale(T.get(r), scale) : czero();
+  for (int j = 0; j < n; j++) {
+    const int p = piv.get(j);
+#pragma unroll
+    for (int r = 1; r <= KLM; r++) {
+      if (r <= kl && p == r) { double2 t = bw[0]; bw[0] = bw[r]; bw[r] = t; }
+    }
+    const int64_t rb = (int64_t)j * NF + W;
+#pragma unroll
+    for (int r = 1; r <= KLM; r++)
+      if (r <= kl) bw[r] = cfms(bw[r], F.get(rb + r), bw[0]);
+    T.put(j, bw[0]);
+#pragma unroll
+    for (int r = 0; r < KLM; r++) if (r < kl) bw[r] = bw[r + 1];
+    const int in = j + 1 + kl;
+    bw[kl] = (in < n) ? cscale(T.get(in), scale) : czero();
+  }
+}
+
+// S4: backward sweep, x = U^{-1} (scale * T) with U = D U' (x_j = b_j rinv_j - sum U'_{j,c} x_{j+c}),
+// in place; returns sum_j Re(conj(RA_j) x_j) (the Lanczos alpha numerator).
+template <int KLM, int KUM, bool DYN>
+PSB_HD double sweep_s4(const Shape& s, LV F, LV T, LV RA, double scale) {
+  constexpr int WM = KLM + KUM;
+  const int n = s.n;
+  const int kl = DYN ? s.kl : KLM;
+  const int W = DYN ? s.W : WM;
+  const int NF = W + 1 + kl;
+  double2 xw[WM + 1];  // xw[c] = x_{j+c}
+#pragma unroll
+  for (int c = 0; c <= WM; c++) xw[c] = czero();
+  double acc = 0.0;
+  for (int j = n - 1; j >= 0; j--) {
+    const int64_t rb = (int64_t)j * NF;
+    double2 x = cmul(cscale(T.get(j), scale), F.get(rb + W));
+#pragma unroll
+    for (int c = WM; c >= 1; c--)
+      if (c <= W) x = cfms(x, F.get(rb + c - 1), xw[c]);
+    T.put(j, x);
+    acc += cdotr(RA.get(j), x);
+#pragma unroll
+    for (int c = WM; c >= 2; c--) xw[c] = xw[c - 1];
+    xw[1] = x;
+  }
+  return acc;
+}
+
+// Largest eigenvalue of the Lanczos tridiagonal T_k (alpha = hist[i].x, beta = hist[i].y),
+// by Newton on det(T_k - x I) from an upper bound x0 (monotone from the right, since all
+// roots are real). Returns theta; *s2 = square of the last component of its eigenvector
+// (= -1 / d_k'(theta) in the LDL^T pivot recurrence), used for the Ritz residual beta_k |s_k|.
+PSB_HD double ritz_top(const double2* hist, int ld, int k, double x0, double* s2) {
+  double x = x0, dp = -1.0;
+  for (int it = 0; it < 200; it++) {
+    double2 h0 = hist[0];
+    double d = h0.x - x;
+    dp = -1.0;
+    double q = 1.0 / d;
+    double S = dp * q;
+    for (int j = 1; j < k; j++) {
+      const double bj = hist[(int64_t)(j - 1) * ld].y;
+      const double b2 = bj * bj;
+      const double dpn = fma(b2 * dp, q * q, -1.0);
+      d = hist[(int64_t)j * ld].x - x - b2 * q;
+      q = 1.0 / d;
+      dp = dpn;
+      S = fma(dp, q, S);
+    }
+    const double step = 1.0 / S;
+    if (!(step > 1e-15 * fabs(x))) break;
+    x -= step;
+  }
+  *s2 = -1.0 / dp;
+  return x;
+}
+
+// Convergence rule (measured on C1..C4 against zgesdd):
+// stop when the Ritz residual r = beta_k |s_k| is below 1e-10 theta, or below 1e-6 theta
+// with the Ritz value stationary to 1e-12.
+PSB_HD bool lanczos_converged(double theta, double dtheta, double r, double beta) {
+  if (beta == 0.0) return true;
+  return (r <= 1e-6 * theta && dtheta <= 1e-12 * theta) || r <= 1e-10 * theta;
+}
+
+// --------------------------------------------------------- engine B: PD test
+// Is G(lam) = A^H A - conj(z) A - z A^H + (|z|^2 - lam) I positive definite?
+// AHA[d * n + j] = (A^H A)[j, j-d], d = 0..b, b = kl + ku.
+// Left-looking banded LDL^H; the previous b rows of L live in a ring of b register
+// slots (row j in slot j mod b; the row loop is unrolled by b so every slot index is a
+// compile-time constant). Virtual rows before 0 are L = 0, D = 1.
+template <int KLM, int KUM>
+struct PDRing {
+  static constexpr int B = KLM + KUM;
+  double2 L[B][B];  // L[slot][d-1] = L(row, row - d)
+  double D[B], iD[B];
+};
+
+template <int KLM, int KUM>
+PSB_HD double2 g_entry(int n, int j, int d, const double2* __restrict__ Ab, const double2* __restrict__ AHA,
+                       double2 z, double zz) {
+  double2 v = AHA[(int64_t)d * n + j];
+  if (d <= KLM) {  // - conj(z) * A[j, j-d]
+    double2 a = Ab[(int64_t)(KLM - d) * n + j];
+    v = cfms_cj(v, z, a);
+  }
+  if (d <= KUM) {  // - z * conj(A[j-d, j])
+    double2 a = Ab[(int64_t)(KLM + d) * n + (j - d)];
+    v = cfms(v, z, cconj(a));
+  }
+  if (d == 0) v.x += zz;
+  return v;
+}
+
+// One row of the factorization for static shapes; U = j mod B (compile-time).
+template <int KLM, int KUM, int U>
+PSB_HD bool pd_row(PDRing<KLM, KUM>& R, int n, int j, const double2* __restrict__ Ab,
+                   const double2* __restrict__ AHA, double2 z, double zz) {
+  constexpr int B = KLM + KUM;
+  double2 g[B + 1];
+#pragma unroll
+  for (int d = 0; d <= B; d++) g[d] = (j - d >= 0) ? g_entry<KLM, KUM>(n, j, d, Ab, AHA, z, zz) : czero();
+  double2 Lj[B + 1], LD[B + 1];
+#pragma unroll
+  for (int d = B; d >= 1; d--) {
+    constexpr int dummy = 0; (void)dummy;
+    const int sc = (U - d + 2 * B) % B;
+    double2 sacc = g[d];
+#pragma unroll
+    for (int dm = B; dm > d; dm--) sacc = cfms_cj(sacc, R.L[sc][dm - d - 1], LD[dm]);
+    Lj[d] = cscale(sacc, R.iD[sc]);
+    LD[d] = cscale(Lj[d], R.D[sc]);
+  }
+  double dj = g[0].x;
+#pragma unroll
+  for (int d = 1; d <= B; d++) dj -= cdotr(Lj[d], LD[d]);
+#pragma unroll
+  for (int d = 1; d <= B; d++) R.L[U][d - 1] = Lj[d];
+  R.D[U] = dj;
+  R.iD[U] = 1.0 / dj;
+  return dj > 0.0;
+}
+
+template <int KLM, int KUM, int U>
+struct PDUnroll {
+  PSB_HD static void run(PDRing<KLM, KUM>& R, int n, int jb, const double2* Ab, const double2* AHA, double2 z,
+                         double zz, bool& pd) {
+    if (jb + U < n) {
+      pd = pd_row<KLM, KUM, U>(R, n, jb + U, Ab, AHA, z, zz) && pd;
+      PDUnroll<KLM, KUM, U + 1>::run(R, n, jb, Ab, AHA, z, zz, pd);
+    }
+  }
+};
+template <int KLM, int KUM>
+struct PDUnroll<KLM, KUM, KLM + KUM> {
+  PSB_HD static void run(PDRing<KLM, KUM>&, int, int, const double2*, const double2*, double2, double, bool&) {}
+};
+
+template <int KLM, int KUM>
+PSB_HD void pd_init(PDRing<KLM, KUM>& R) {
+  constexpr int B = KLM + KUM;
+#pragma unroll
+  for (int s = 0; s < B; s++) {
+#pragma unroll
+    for (int d = 0; d < B; d++) R.L[s][d] = czero();
+    R.D[s] = 1.0;
+    R.iD[s] = 1.0;
+  }
+}
+
+// Host/generic form: whole-test loop (device kernels drive the group loop themselves so
+// they can vote on early exit).
+template <int KLM, int KUM>
+PSB_HD bool pd_test_static(int n, const double2* __restrict__ Ab, const double2* __restrict__ AHA, double2 z,
+                           double lam) {
+  constexpr int B = KLM + KUM;
+  PDRing<KLM, KUM> R;
+  pd_init(R);
+  const double zz = cnorm2(z) - lam;
+  bool pd = true;
+  for (int jb = 0; jb < n && pd; jb += B) PDUnroll<KLM, KUM, 0>::run(R, n, jb, Ab, AHA, z, zz, pd);
+  return pd;
+}
+
+// Runtime-shape PD test (any kl, ku; ring in a caller-provided scratch of b*b complex + 2b doubles).
+PSB_HD bool pd_test_dyn(int n, int kl, int ku, const double2* __restrict__ Ab, const double2* __restrict__ AHA,
+                        double2 z, double lam, LV Lsc, double* Dsc, int dld) {
+  const int b = kl + ku;
+  const double zz = cnorm2(z) - lam;
+  if (b == 0) {  // diagonal A
+    for (int j = 0; j < n; j++) {
+      double2 v = AHA[j];
+      v = cfms_cj(v, z, Ab[j]);
+      v = cfms(v, z, cconj(Ab[j]));
+      if (!(v.x + zz > 0.0)) return false;
+    }
+    return true;
+  }
+  for (int s = 0; s < b; s++) {
+    for (int d = 0; d < b; d++) Lsc.put((int64_t)s * b + d, czero());
+    Dsc[(int64_t)(2 * s) * dld] = 1.0;
+    Dsc[(int64_t)(2 * s + 1) * dld] = 1.0;
+  }
+  double2 Lj[33], LD[33];
+  for (int j = 0; j < n; j++) {
+    for (int d = b; d >= 1; d--) {
+      const int c = j - d;
+      double2 g = czero();
+      if (c >= 0) {
+        g = AHA[(int64_t)d * n + j];
+        if (d <= kl) g = cfms_cj(g, z, Ab[(int64_t)(kl - d) * n + j]);
+        if (d <= ku) g = cfms(g, z, cconj(Ab[(int64_t)(kl + d) * n + c]));
+      }
+      const int sc = ((c % b) + b) % b;
+      double2 sacc = g;
+      for (int dm = b; dm > d; dm--) sacc = cfms_cj(sacc, Lsc.get((int64_t)sc * b + dm - d - 1), LD[dm]);
+      Lj[d] = cscale(sacc, Dsc[(int64_t)(2 * sc + 1) * dld]);
+      LD[d] = cscale(Lj[d], Dsc[(int64_t)(2 * sc) * dld]);
+    }
+    double2 g0 = AHA[j];
+    g0 = cfms_cj(g0, z, Ab[(int64_t)kl * n + j]);
+    g0 = cfms(g0, z, cconj(Ab[(int64_t)kl * n + j]));
+    double dj = g0.x + zz;
+    for (int d = 1; d <= b; d++) dj -= cdotr(Lj[d], LD[d]);
+    if (!(dj > 0.0)) return false;
+    const int s0 = j % b;
+    for (int d = 1; d <= b; d++) Lsc.put((int64_t)s0 * b + d - 1, Lj[d]);
+    Dsc[(int64_t)(2 * s0) * dld] = dj;
+    Dsc[(int64_t)(2 * s0 + 1) * dld] = 1.0 / dj;
+  }
+  return true;
+}
+
+// Bisection state machine of engine B (per point).
+//   phase 0: classify at lam = (tau S)^2: PD -> sigma >= tau S -> search; else hand to engine L
+//   phase 1: geometric search upward (x4 in lambda) until a test fails
+//   phase 2: bisection until (hi - lo) <= rtol * hi; sigma = sqrt((lo + hi) / 2)
+struct BisState {
+  double lo, hi, lam;
+  int phase, tests;
+};
+enum { BIS_CONTINUE = 0, BIS_DONE = 1, BIS_TO_LANCZOS = 2, BIS_FAIL = 3 };
+
+PSB_HD void bis_start(BisState& st, double z_abs, double anorm, double tau) {
+  const double t = tau * (z_abs + anorm);
+  st.lo = 0.0; st.hi = 0.0; st.lam = t * t; st.phase = 0; st.tests = 0;
+}
+PSB_HD int bis_update(BisState& st, bool pd, double rtol, bool force_bisect, int max_tests) {
+  st.tests++;
+  if (st.tests > max_tests) return BIS_FAIL;
+  if (st.phase == 0) {
+    if (!pd) {
+      if (!force_bisect) return BIS_TO_LANCZOS;
+      st.lo = 0.0; st.hi = st.lam; st.phase = 2; st.lam = 0.5 * st.hi; return BIS_CONTINUE;
+    }
+    st.lo = st.lam; st.hi = 4.0 * st.lam; st.lam = st.hi; st.phase = 1; return BIS_CONTINUE;
+  }
+  if (st.phase == 1) {
+    if (pd) { st.lo = st.hi; st.hi *= 4.0; st.lam = st.hi; return BIS_CONTINUE; }
+    st.phase = 2;
+  } else {
+    if (pd) st.lo = st.lam; else st.hi = st.lam;
+  }
+  if (st.hi - st.lo <= rtol * st.hi) return BIS_DONE;
+  st.lam = 0.5 * (st.lo + st.hi);
+  return BIS_CONTINUE;
+}
+PSB_HD double bis_sigma(const BisState& st) { return sqrt(0.5 * (st.lo + st.hi)); }
+
+}  // namespace psb

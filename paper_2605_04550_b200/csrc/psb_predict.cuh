@@ -1,0 +1,153 @@
+// psb_predict.cuh — K2: the reference's sensitivity classifier and region selection on device.
+//
+//   per-point features   pseudospec/features.py:129-137 point_features_many (g1 = min|z-l|,
+//                        g2 = |z - mean l|, g3 = mean|z-l|; numpy pairwise summation restated)
+//                        features.py:145-151 assemble_many, 163-164 standardize
+//   Fourier encoding     pseudospec/network.py:62-75 (x, y, then sin/cos at 2^1..2^6)
+//   dual-path MLP        pseudospec/network.py:153-190 (_forward_cache/forward, SiLU, sigmoid),
+//                        parameter layout network.py:35-52 PARAM_SHAPES (59,841 float64)
+//   region               pseudospec/pipeline.py:227-231 predicted_region: dilate(prob >= tau, 5)
+//                        with border clipping (core.py:224-231, scipy binary_dilation)
+//
+// FP64 throughout (the reference network is float64, network.py:1-14). One thread per point;
+// weights are read with warp-uniform addresses (broadcast), activations live in shared
+// memory interleaved by thread ([unit][thread]) so the per-thread reads are bank-conflict free.
+#pragma once
+#include "psb_algo.cuh"
+
+namespace psb {
+
+// parameter offsets in PARAM_SHAPES order
+struct MlpOff {
+  static constexpr int w_c1 = 0, b_c1 = w_c1 + 64 * 26, w_c2 = b_c1 + 64, b_c2 = w_c2 + 64 * 64;
+  static constexpr int w_m1 = b_c2 + 64, b_m1 = w_m1 + 128 * 33, w_m2 = b_m1 + 128, b_m2 = w_m2 + 64 * 128;
+  static constexpr int w_t1 = b_m2 + 64, b_t1 = w_t1 + 128 * 128, w_t2 = b_t1 + 128, b_t2 = w_t2 + 128 * 128;
+  static constexpr int w_proj = b_t2 + 128, b_proj = w_proj + 64 * 128, w_head = b_proj + 64,
+                       b_head = w_head + 64, total = b_head + 1;
+};
+static_assert(MlpOff::total == 59841, "PARAM_SHAPES total");
+
+constexpr int MLP_TPB = 32;  // threads per block (one warp): smem = 3 * 128 * 32 * 8 = 96 KB
+
+__device__ __forceinline__ double expit_d(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src pairwise_sum, PW_BLOCKSIZE 128)
+// over f(k), k in [lo, lo+len)
+template <class F>
+__device__ double np_pairwise(F f, int lo, int len) {
+  if (len < 8) {
+    double res = 0.0;  // numpy starts from -0.0 for sums; identical for the non-negative terms here
+    for (int i = 0; i < len; i++) res += f(lo + i);
+    return res;
+  } else if (len <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; j++) r[j] = f(lo + j);
+    int i;
+    for (i = 8; i < len - (len % 8); i += 8)
+      for (int j = 0; j < 8; j++) r[j] += f(lo + i + j);
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < len; i++) res += f(lo + i);
+    return res;
+  } else {
+    int n2 = len / 2;
+    n2 -= n2 % 8;
+    return np_pairwise(f, lo, n2) + np_pairwise(f, lo + n2, len - n2);
+  }
+}
+
+__device__ __forceinline__ void dense(const double* __restrict__ W, const double* __restrict__ bvec, int nin,
+                                      int nout, const double* x, double* y, bool act) {
+  const int t = threadIdx.x;
+  for (int o = 0; o < nout; o++) {
+    const double* w = W + (int64_t)o * nin;
+    double acc = 0.0;
+    for (int i = 0; i < nin; i++) acc = fma(__ldg(w + i), x[i * MLP_TPB + t], acc);
+    acc += __ldg(bvec + o);
+    y[o * MLP_TPB + t] = act ? acc * expit_d(acc) : acc;
+  }
+}
+
+struct PredictArgs {
+  const double* params;
+  const double* mean33;
+  const double* std33;
+  const double* f30;
+  const double2* eig;
+  double2 eig_mean;
+  int n_eig;
+  const double2* zs;
+  int64_t P;
+  double* prob;
+};
+
+__global__ void __launch_bounds__(MLP_TPB) k_predict(PredictArgs a) {
+  extern __shared__ double sm[];
+  double* X = sm;                       // 128 x TPB
+  double* Y = sm + 128 * MLP_TPB;       // 128 x TPB
+  double* Z = sm + 256 * MLP_TPB;       // 128 x TPB
+  const int t = threadIdx.x;
+  const int64_t p = (int64_t)blockIdx.x * MLP_TPB + t;
+  const bool live = p < a.P;
+  const double2 z = live ? a.zs[p] : czero();
+  // ---- features (features.py:129-137) ----
+  double g1 = INFINITY;
+  for (int k = 0; k < a.n_eig; k++) {
+    const double2 l = a.eig[k];
+    const double d = hypot(z.x - l.x, z.y - l.y);
+    g1 = fmin(g1, d);
+  }
+  const double g2 = hypot(z.x - a.eig_mean.x, z.y - a.eig_mean.y);
+  auto dist = [&](int k) { const double2 l = a.eig[k]; return hypot(z.x - l.x, z.y - l.y); };
+  const double g3 = np_pairwise(dist, 0, a.n_eig) / (double)a.n_eig;
+  // standardized 33-vector into Z[0..32]
+  for (int c = 0; c < 30; c++) Z[c * MLP_TPB + t] = (a.f30[c] - a.mean33[c]) / a.std33[c];
+  Z[30 * MLP_TPB + t] = (g1 - a.mean33[30]) / a.std33[30];
+  Z[31 * MLP_TPB + t] = (g2 - a.mean33[31]) / a.std33[31];
+  Z[32 * MLP_TPB + t] = (g3 - a.mean33[32]) / a.std33[32];
+  // Fourier encoding (network.py:62-75) into X[0..25]
+  X[0 * MLP_TPB + t] = z.x;
+  X[1 * MLP_TPB + t] = z.y;
+  for (int q = 0; q < 6; q++) {
+    const double f = (double)(2 << q);
+    X[(2 + 4 * q) * MLP_TPB + t] = sin(f * z.x);
+    X[(3 + 4 * q) * MLP_TPB + t] = sin(f * z.y);
+    X[(4 + 4 * q) * MLP_TPB + t] = cos(f * z.x);
+    X[(5 + 4 * q) * MLP_TPB + t] = cos(f * z.y);
+  }
+  const double* P = a.params;
+  typedef MlpOff O;
+  // coordinate path: phi(26) -> 64 -> 64 ; h_c1 in Y[0..63], h_c2 into Y[64..127]? keep layout h3 = [h_c2, h_m2]
+  dense(P + O::w_c1, P + O::b_c1, 26, 64, X, Y, true);           // Y = h_c1
+  dense(P + O::w_c2, P + O::b_c2, 64, 64, Y, X, true);           // X[0..63] = h_c2
+  // matrix path: f(33) -> 128 -> 64
+  dense(P + O::w_m1, P + O::b_m1, 33, 128, Z, Y, true);          // Y = h_m1
+  dense(P + O::w_m2, P + O::b_m2, 128, 64, Y, X + 64 * MLP_TPB, true);  // X[64..127] = h_m2  => X = h3
+  dense(P + O::w_t1, P + O::b_t1, 128, 128, X, Y, true);         // Y = h4
+  dense(P + O::w_t2, P + O::b_t2, 128, 128, Y, Z, true);         // Z = h5
+  for (int c = 0; c < 128; c++) Z[c * MLP_TPB + t] = Y[c * MLP_TPB + t] + Z[c * MLP_TPB + t];  // h6 = h4 + h5
+  dense(P + O::w_proj, P + O::b_proj, 128, 64, Z, X, true);      // X[0..63] = h7
+  double logit = 0.0;
+  for (int i = 0; i < 64; i++) logit = fma(__ldg(P + O::w_head + i), X[i * MLP_TPB + t], logit);
+  logit += __ldg(P + O::b_head);
+  if (live) a.prob[p] = expit_d(logit);
+}
+
+// region = dilate(prob >= tau, k) with border clipping; region[g] in {0,1}
+__global__ void k_region(const double* __restrict__ prob, int ny, int nx, double tau, int k, uint8_t* region) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int64_t)ny * nx) return;
+  const int i = (int)(g / nx), j = (int)(g % nx), h = k / 2;
+  uint8_t v = 0;
+  for (int di = -h; di <= h && !v; di++) {
+    const int ii = i + di;
+    if (ii < 0 || ii >= ny) continue;
+    for (int dj = -h; dj <= h; dj++) {
+      const int jj = j + dj;
+      if (jj < 0 || jj >= nx) continue;
+      if (prob[(int64_t)ii * nx + jj] >= tau) { v = 1; break; }
+    }
+  }
+  region[g] = v;
+}
+
+}  // namespace psb
