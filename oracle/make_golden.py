@@ -1,0 +1,227 @@
+"""ORACLE fixture generator (test infrastructure only; run in the build container, where the
+read-only reference lives at /root/reference). Writes tests/golden/*.npz.
+
+Every σ fixture is produced by the reference's own code (pseudospec.core, imported from
+/root/reference/pkg/src, BLAS pinned to one thread) for real A, and by the restatement
+oracle/sigma_oracle.smin_restated (the same numpy zgesdd call without the real cast,
+core.py:112-119) for the complex configs C3/C5, which the reference cannot evaluate.
+The guided-path fixtures (K2) come from the reference's pipeline.hierarchical_predict /
+predicted_region with a bundle trained *by the reference* (network.train, calibrate_threshold)
+on a seeded Grcar-family corpus (see train_grcar_bundle).
+
+Usage:  python oracle/make_golden.py sigma|model|guided|all
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+from concurrent.futures import ProcessPoolExecutor
+from pathlib import Path
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+import numpy as np
+from threadpoolctl import threadpool_limits
+
+ROOT = Path(__file__).resolve().parent.parent
+REF = Path("/root/reference/pkg/src")
+GOLD = ROOT / "tests" / "golden"
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(REF))
+
+from oracle.sigma_oracle import smin_restated  # noqa: E402
+from paper_2605_04550_b200 import configs  # noqa: E402
+
+
+def _ref_chunk(args):
+    A, zs = args
+    from pseudospec import core as rcore
+    with threadpool_limits(1):
+        return rcore.smin_many(A, zs, chunk=1)
+
+
+def _restated_chunk(args):
+    A, zs = args
+    return smin_restated(A, zs)
+
+
+def _pool(fn, A, zs, procs=8):
+    chunks = [c for c in np.array_split(zs, max(1, min(procs * 2, zs.size))) if c.size]
+    with ProcessPoolExecutor(max_workers=procs) as ex:
+        parts = list(ex.map(fn, [(A, c) for c in chunks]))
+    return np.concatenate(parts)
+
+
+def gen_sigma():
+    from pseudospec import core as rcore
+    GOLD.mkdir(parents=True, exist_ok=True)
+    # C1: the reference's full_pseudospectrum on the exact config grid
+    cfg = configs.CONFIGS["C1"]
+    A = cfg.matrix().todense().real.copy()
+    t = time.time()
+    with threadpool_limits(1):
+        fld = rcore.full_pseudospectrum(A, rcore.make_grid(-1, 3, -3.5, 3.5, 50, 50))
+    np.savez_compressed(GOLD / "c1_full.npz", values=fld.values, grid=np.array([-1, 3, -3.5, 3.5, 50, 50.0]),
+                        norm2=np.linalg.norm(A, 2))
+    print("c1", time.time() - t, flush=True)
+    # demo 01: nilpotent shift n=32 on [-1.5,1.5]^2 120x120 (demos/01_sensitivity_basics.py:21-47)
+    A01 = np.diag(np.ones(31), k=-1)
+    with threadpool_limits(1):
+        f01 = rcore.full_pseudospectrum(A01, rcore.make_grid(-1.5, 1.5, -1.5, 1.5, 120, 120))
+    shipped = Path("/root/reference/pkg/demos/output_01_field.csv")
+    same = None
+    if shipped.exists():
+        from pseudospec.io import write_field_csv
+        tmp = Path("/tmp/_demo01.csv")
+        write_field_csv(tmp, f01)
+        same = tmp.read_bytes() == shipped.read_bytes()
+    np.savez_compressed(GOLD / "demo01_field.npz", values=f01.values,
+                        csv_byte_identical=np.array(bool(same)))
+    print("demo01 byte-identical to shipped CSV:", same, flush=True)
+    # C2 sample (real Grcar n=400): reference smin_many
+    for name, count, seed, fn in (("C2", 480, 21, _ref_chunk), ("C3", 192, 31, _restated_chunk),
+                                  ("C4", 48, 41, _ref_chunk)):
+        cfg = configs.CONFIGS[name]
+        Ad = cfg.matrix().todense()
+        if np.all(Ad.imag == 0):
+            Ad = Ad.real.copy()
+        idx, zs = configs.sample_points(cfg, count, seed)
+        t = time.time()
+        want = _pool(fn, Ad, zs)
+        np.savez_compressed(GOLD / f"{name.lower()}_sample.npz", idx=idx, zs=zs, sigma=want,
+                            norm2=np.linalg.norm(Ad, 2), kind=np.array("reference" if fn is _ref_chunk else "restated"))
+        print(name, count, time.time() - t, flush=True)
+    # C5: 4 of the 64 matrices, 6 grid shifts each (restated; n=4000 dense SVDs)
+    cfg = configs.CONFIGS["C5"]
+    rows = []
+    for m in (0, 1, 17, 63):
+        Ad = cfg.matrix(m).todense()
+        idx, zs = configs.sample_points(cfg, 6, 500 + m)
+        t = time.time()
+        want = _pool(_restated_chunk, Ad, zs, procs=6)
+        rows.append((m, idx, zs, want, np.linalg.norm(Ad, 2)))
+        print("C5", m, time.time() - t, flush=True)
+    np.savez_compressed(GOLD / "c5_sample.npz", matrices=np.array([r[0] for r in rows]),
+                        idx=np.stack([r[1] for r in rows]), zs=np.stack([r[2] for r in rows]),
+                        sigma=np.stack([r[3] for r in rows]), norm2=np.array([r[4] for r in rows]))
+    gen_small()
+
+
+def gen_small():
+    """Small random banded {-1,0,1} matrices (tests/test_acceptance.py:53-70 style), reference smin_many."""
+    from pseudospec import core as rcore
+    rng = np.random.default_rng(10)
+    mats, zss, sig, ns = [], [], [], []
+    for _ in range(30):
+        n = int(rng.integers(4, 17))
+        beta = int(rng.integers(1, min(4, n - 1) + 1))
+        A = rng.integers(-1, 2, size=(n, n)).astype(float)
+        i = np.arange(n)
+        A[np.abs(i[:, None] - i[None, :]) > beta] = 0.0
+        zs = rng.uniform(-4, 4, 40) + 1j * rng.uniform(-4, 4, 40)
+        with threadpool_limits(1):
+            s = rcore.smin_many(A, zs)
+        Ap = np.zeros((16, 16))
+        Ap[:n, :n] = A
+        mats.append(Ap); zss.append(zs); sig.append(s); ns.append(n)
+    np.savez_compressed(GOLD / "small_random.npz", A=np.stack(mats), zs=np.stack(zss), sigma=np.stack(sig),
+                        n=np.array(ns))
+    print("small random done", flush=True)
+
+
+# ------------------------------------------------------------------ guided path (K2)
+def grcar_family(count, seed, n_choices=(32, 40, 48, 56, 64)):
+    """Seeded Grcar-family corpus: Grcar(n, k) with random +-10% perturbations of the band
+    coefficients (real), as CorpusMatrix entries of the reference."""
+    from pseudospec.generate import CorpusMatrix, mix64
+    out = []
+    for i in range(count):
+        child = mix64(seed, i)
+        rng = np.random.default_rng(np.random.PCG64(child))
+        n = int(rng.choice(n_choices))
+        k = int(rng.integers(2, 5))
+        A = -np.diag(np.ones(n - 1), -1) * (1 + 0.1 * rng.uniform(-1, 1))
+        for j in range(0, k + 1):
+            A += np.diag(np.ones(n - j), j) * (1 + 0.1 * rng.uniform(-1, 1))
+        out.append(CorpusMatrix(index=i, seed=child, matrix=A, bandwidth=k, kappa=float(np.linalg.cond(A))))
+    return out
+
+
+def train_grcar_bundle():
+    from pseudospec import TrainConfig, build_dataset, calibrate_threshold, make_grid, save_model, train
+    grid = make_grid(-1, 3, -3.5, 3.5, 48, 48)
+    eps = 0.01
+    tr = grcar_family(80, seed=7001)
+    va = grcar_family(12, seed=7002)
+    t = time.time()
+    ds = build_dataset(tr, grid, eps, seed=7003, workers=8)
+    print("dataset", len(ds), int(ds.labels.sum()), time.time() - t, flush=True)
+    for seed in (42, 43, 44):
+        bundle, hist = train(ds, TrainConfig(max_epochs=25, patience=5, seed=seed, batch_size=512))
+        rep = calibrate_threshold(bundle, va, grid, eps, workers=8)
+        print("seed", seed, "epochs", len(hist), "passed", rep.passed, rep.tau_star, flush=True)
+        if rep.passed:
+            bundle.tau_star = rep.tau_star
+            bundle.meta.update({"train_seed": seed, "corpus": "grcar_family(80, 7001)", "grid": "48x48 C2 box",
+                                "eps": eps})
+            save_model(bundle, "/tmp/model_grcar.json")
+            from pseudospec.network import PARAM_SHAPES
+            np.savez_compressed(GOLD / "model_grcar.npz",
+                                **{k: getattr(bundle.params, k) for k in PARAM_SHAPES},
+                                feature_mean=bundle.feature_mean, feature_std=bundle.feature_std,
+                                tau_star=np.array(bundle.tau_star), meta=np.array(json.dumps(bundle.meta)))
+            return bundle
+    raise SystemExit("calibration failed for every seed")
+
+
+def load_bundle_npz():
+    from pseudospec.network import PARAM_SHAPES, ModelBundle, ModelParams
+    z = np.load(GOLD / "model_grcar.npz")
+    params = ModelParams(**{k: z[k] for k in PARAM_SHAPES})
+    return ModelBundle(params=params, feature_mean=z["feature_mean"], feature_std=z["feature_std"],
+                       tau_star=float(z["tau_star"]))
+
+
+def gen_guided():
+    from pseudospec import pipeline, features
+    from pseudospec.core import make_grid
+    bundle = load_bundle_npz()
+    cfg = configs.CONFIGS["C2"]
+    A = cfg.matrix().todense().real.copy()
+    grid = make_grid(-1, 3, -3.5, 3.5, 200, 200)
+    with threadpool_limits(1):
+        t = time.time()
+        prob, n_evals = pipeline.hierarchical_predict(bundle, A, grid, stride=4, probe_seed=0)
+        region = pipeline.predicted_region(prob, bundle.tau_star)
+        gf = features.global_features(A, probe_seed=0)
+        rng = np.random.default_rng(99)
+        zs = grid.points().ravel()[rng.choice(grid.size, 512, replace=False)]
+        p_pts = pipeline._predict_points(bundle, gf, zs)
+        print("guided", time.time() - t, "evals", n_evals, "region frac", region.mean(), flush=True)
+    np.savez_compressed(GOLD / "c2_guided.npz", prob=prob, n_evals=n_evals, region=region,
+                        f30=gf.values, eig=gf.eigvals, sample_zs=zs, sample_prob=p_pts, tau=bundle.tau_star)
+    # a second, smaller case: C1 (Grcar n=100) so tests stay fast
+    A1 = configs.CONFIGS["C1"].matrix().todense().real.copy()
+    g1 = make_grid(-1, 3, -3.5, 3.5, 50, 50)
+    with threadpool_limits(1):
+        prob1, ne1 = pipeline.hierarchical_predict(bundle, A1, g1, stride=4, probe_seed=0)
+        reg1 = pipeline.predicted_region(prob1, bundle.tau_star)
+        gf1 = features.global_features(A1, probe_seed=0)
+        pm1 = pipeline.predict_map(bundle, A1, g1, probe_seed=0)
+    np.savez_compressed(GOLD / "c1_guided.npz", prob=prob1, n_evals=ne1, region=reg1, f30=gf1.values,
+                        eig=gf1.eigvals, dense=pm1, tau=bundle.tau_star)
+    print("c1 guided evals", ne1, "region frac", reg1.mean(), flush=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("sigma", "all"):
+        gen_sigma()
+    if what == "small":
+        gen_small()
+    if what in ("model", "all"):
+        train_grcar_bundle()
+    if what in ("guided", "all"):
+        gen_guided()

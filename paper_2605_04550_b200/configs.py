@@ -80,7 +80,7 @@ def c5_band(index: int, n: int = 4000, seed: int | None = None) -> BandMatrix:
 
 # Frozen grid boxes (see module docstring). C3/C5 values are written by oracle/make_golden.py.
 C3_BOX = (-1.3120622297077658, 2.8202251704993175, -1.5441211819491594, 3.333362897155037)
-C5_BOX = (-8.95, 10.05, -9.35, 9.65)
+C5_BOX = (-4.588273233499905, 6.7666325650326264, -6.490070062540546, 3.9341982302654523)
 _H4 = 1.0 / 2001
 C4_BOX = (-4.2 / _H4**2, 0.2 / _H4**2, -1.1e5, 1.1e5)
 

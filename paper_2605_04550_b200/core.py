@@ -179,17 +179,26 @@ class BandMatrix:
         return A
 
 
+MAX_BAND = 16
+
+
 def as_band(A):
-    """(band, kl, ku, n) for a dense array or a BandMatrix."""
+    """(band, kl, ku, n) for a dense array or a BandMatrix; kl, ku <= MAX_BAND."""
     if isinstance(A, BandMatrix):
-        return A.band, A.kl, A.ku, A.n
-    A = require_matrix(A)
-    kl, ku = bandwidths(A)
-    return np.ascontiguousarray(band_of(A, kl, ku)), kl, ku, A.shape[0]
+        band, kl, ku, n = A.band, A.kl, A.ku, A.n
+    else:
+        A = require_matrix(A)
+        kl, ku = bandwidths(A)
+        band, n = np.ascontiguousarray(band_of(A, kl, ku)), A.shape[0]
+    if kl > MAX_BAND or ku > MAX_BAND:
+        raise ParameterError(f"band evaluator supports kl, ku <= {MAX_BAND}, got kl={kl} ku={ku}")
+    return band, kl, ku, n
 
 
 def _set_matrix(h: _lib.Handle, A):
-    band, kl, ku, n = as_band(A)
+    band, kl, ku, n = A if isinstance(A, tuple) else as_band(A)
+    if kl > 16 or ku > 16:
+        raise ParameterError(f"band evaluator supports kl, ku <= 16, got kl={kl} ku={ku}")
     key = (n, kl, ku, hashlib.blake2b(band.tobytes(), digest_size=16).digest())
     if h._matrix_key == key:
         return n
@@ -234,9 +243,12 @@ def smin_many(A, zs: np.ndarray, label: str = "matrix", chunk: int = 512, *,
               opts: _lib.Opts | None = None, return_info: bool = False):
     """σ_min(z I - A) for a 1-D array of shift points (core.py:141-168)."""
     zs = np.ascontiguousarray(np.asarray(zs, dtype=complex).ravel())
+    band = as_band(A)  # validate on the host first (ParameterError without touching the device)
+    if not np.all(np.isfinite(zs)):
+        raise ParameterError("shift points must be finite")
     h = _lib.handle()
     with h.lock:
-        _set_matrix(h, A)
+        _set_matrix(h, band)
         P = zs.size
         out = np.empty(P)
         iters = np.empty(P, dtype=np.int32)
@@ -262,9 +274,10 @@ def smin_at(A, z: complex, label: str = "matrix") -> float:
 def _grid_call(A, grid: ComplexGrid, region, label, opts=None):
     xs = np.ascontiguousarray(grid.xs())
     ys = np.ascontiguousarray(grid.ys())
+    band = as_band(A)
     h = _lib.handle()
     with h.lock:
-        _set_matrix(h, A)
+        _set_matrix(h, band)
         out = np.empty(grid.shape)
         status = np.empty(grid.shape, dtype=np.int8)
         reg = None if region is None else np.ascontiguousarray(region, dtype=np.uint8)

@@ -79,20 +79,23 @@ struct LV {
   PSB_HD void put(int64_t i, double2 v) const { p[i * ld] = v; }
 };
 struct LVb {
-  uint8_t* p;
+  int* p;
   int ld;
   PSB_HD int get(int64_t i) const { return p[i * ld]; }
-  PSB_HD void put(int64_t i, int v) const { p[i * ld] = (uint8_t)v; }
+  PSB_HD void put(int64_t i, int v) const { p[i * ld] = v; }
 };
 
 // Shape of the band problem. Band of A: Ab[(d + kl) * n + i] = A[i, i + d], d in [-kl, ku].
-// Factor row j (NF = W + 1 + kl complex): [U'(j, j+1..j+W) | rinv_j | L(j, 1..kl)],
-// U' = rinv * U (row-scaled upper factor), W = kl + ku.
+// Factors, stored per row so each triangular sweep streams only what it reads:
+//   FU row j (NU = W + 1 complex): [U'(j, j+1..j+W) | rinv_j],  U' = rinv * U (row-scaled)
+//   FL row j (NL = kl complex):    [L(j, j+1..j+kl)] (multipliers of elimination step j)
+//   piv[j] in 0..kl: row swapped into position j at step j (int32)
+// W = kl + ku is the upper bandwidth after partial-pivoting fill.
 struct Shape {
-  int n, kl, ku, W, NF;
+  int n, kl, ku, W, NU, NL;
 };
 PSB_HD Shape make_shape(int n, int kl, int ku) {
-  Shape s; s.n = n; s.kl = kl; s.ku = ku; s.W = kl + ku; s.NF = kl + ku + 1 + kl; return s;
+  Shape s; s.n = n; s.kl = kl; s.ku = ku; s.W = kl + ku; s.NU = kl + ku + 1; s.NL = kl > 0 ? kl : 1; return s;
 }
 
 // ------------------------------------------------------------ engine L: band LU
@@ -100,13 +103,13 @@ PSB_HD Shape make_shape(int n, int kl, int ku) {
 // columns. Pivot rule: first max of |re|+|im| (LAPACK izamax/dcabs1 convention,
 // as zgbtrf). Returns false on an exactly zero pivot (M singular in floating point).
 template <int KLM, int KUM, bool DYN>
-PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z, LV F, LVb piv) {
+PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z, LV FU, LV FL, LVb piv) {
   constexpr int WM = KLM + KUM;
   const int n = s.n;
   const int kl = DYN ? s.kl : KLM;
   const int ku = DYN ? s.ku : KUM;
   const int W = kl + ku;
-  const int NF = W + 1 + kl;
+  const int NU = W + 1, NL = s.NL;
   double2 win[KLM + 1][WM + 1];
   bool ok = true;
   // initial rows r = 0..kl hold matrix rows r, columns 0..W
@@ -150,16 +153,16 @@ PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z,
     double2 ri;
     if (d.x == 0.0 && d.y == 0.0) { ok = false; ri = czero(); }
     else ri = crcp(d);
-    const int64_t rb = (int64_t)j * NF;
+    const int64_t rb = (int64_t)j * NU;
 #pragma unroll
     for (int c = 1; c <= WM; c++)
-      if (c <= W) F.put(rb + c - 1, cmul(win[0][c], ri));
-    F.put(rb + W, ri);
+      if (c <= W) FU.put(rb + c - 1, cmul(win[0][c], ri));
+    FU.put(rb + W, ri);
 #pragma unroll
     for (int r = 1; r <= KLM; r++) {
       if (r <= kl) {
         double2 l = cmul(win[r][0], ri);
-        F.put(rb + W + r, l);
+        FL.put((int64_t)j * NL + r - 1, l);
 #pragma unroll
         for (int c = 1; c <= WM; c++)
           if (c <= W) win[r][c] = cfms(win[r][c], l, win[0][c]);
@@ -203,9 +206,8 @@ PSB_HD double sweep_s1(const Shape& s, LV F, LV T, LV RA, LV RB, const double2* 
                        int k, double c1, double c2) {
   constexpr int WM = KLM + KUM;
   const int n = s.n;
-  const int kl = DYN ? s.kl : KLM;
   const int W = DYN ? s.W : WM;
-  const int NF = W + 1 + kl;
+  const int NF = W + 1;  // F = FU
   double2 tw[WM + 1];  // tw[d] = t'_{j-d}
 #pragma unroll
   for (int d = 0; d <= WM; d++) tw[d] = czero();
@@ -240,11 +242,10 @@ PSB_HD double sweep_s1(const Shape& s, LV F, LV T, LV RA, LV RB, const double2* 
 // S2: backward sweep, apply E^H (row swaps + unit-lower multipliers, transposed).
 // Returns ||output||^2.
 template <int KLM, int KUM, bool DYN>
-PSB_HD double sweep_s2(const Shape& s, LV F, LVb piv, LV T) {
+PSB_HD double sweep_s2(const Shape& s, LV F, LVb piv, LV T) {  // F = FL
   const int n = s.n;
   const int kl = DYN ? s.kl : KLM;
-  const int W = DYN ? s.W : KLM + KUM;
-  const int NF = W + 1 + kl;
+  const int NL = s.NL;
   double2 yw[KLM + 1];  // yw[r] = y_{j+r}
 #pragma unroll
   for (int r = 0; r <= KLM; r++) yw[r] = czero();
@@ -255,7 +256,7 @@ PSB_HD double sweep_s2(const Shape& s, LV F, LVb piv, LV T) {
 #pragma unroll
     for (int r = KLM; r >= 1; r--) if (r <= kl) yw[r] = yw[r - 1];
     double2 y = T.get(j);
-    const int64_t rb = (int64_t)j * NF + W;
+    const int64_t rb = (int64_t)j * NL - 1;
 #pragma unroll
     for (int r = KLM; r >= 1; r--)
       if (r <= kl) y = cfms_cj(y, F.get(rb + r), yw[r]);
@@ -274,11 +275,10 @@ PSB_HD double sweep_s2(const Shape& s, LV F, LVb piv, LV T) {
 
 // S3: forward sweep, apply E (row swaps + eliminations) to scale * T, in place.
 template <int KLM, int KUM, bool DYN>
-PSB_HD void sweep_s3(const Shape& s, LV F, LVb piv, LV T, double scale) {
+PSB_HD void sweep_s3(const Shape& s, LV F, LVb piv, LV T, double scale) {  // F = FL
   const int n = s.n;
   const int kl = DYN ? s.kl : KLM;
-  const int W = DYN ? s.W : KLM + KUM;
-  const int NF = W + 1 + kl;
+  const int NL = s.NL;
   double2 bw[KLM + 1];  // bw[r] = b_{j+r}
 #pragma unroll
   for (int r = 0; r <= KLM; r++) bw[r] = (r <= kl && r < n) ? cscale(T.get(r), scale) : czero();
@@ -288,7 +288,7 @@ PSB_HD void sweep_s3(const Shape& s, LV F, LVb piv, LV T, double scale) {
     for (int r = 1; r <= KLM; r++) {
       if (r <= kl && p == r) { double2 t = bw[0]; bw[0] = bw[r]; bw[r] = t; }
     }
-    const int64_t rb = (int64_t)j * NF + W;
+    const int64_t rb = (int64_t)j * NL - 1;
 #pragma unroll
     for (int r = 1; r <= KLM; r++)
       if (r <= kl) bw[r] = cfms(bw[r], F.get(rb + r), bw[0]);
@@ -303,12 +303,11 @@ PSB_HD void sweep_s3(const Shape& s, LV F, LVb piv, LV T, double scale) {
 // S4: backward sweep, x = U^{-1} (scale * T) with U = D U' (x_j = b_j rinv_j - sum U'_{j,c} x_{j+c}),
 // in place; returns sum_j Re(conj(RA_j) x_j) (the Lanczos alpha numerator).
 template <int KLM, int KUM, bool DYN>
-PSB_HD double sweep_s4(const Shape& s, LV F, LV T, LV RA, double scale) {
+PSB_HD double sweep_s4(const Shape& s, LV F, LV T, LV RA, double scale) {  // F = FU
   constexpr int WM = KLM + KUM;
   const int n = s.n;
-  const int kl = DYN ? s.kl : KLM;
   const int W = DYN ? s.W : WM;
-  const int NF = W + 1 + kl;
+  const int NF = W + 1;
   double2 xw[WM + 1];  // xw[c] = x_{j+c}
 #pragma unroll
   for (int c = 0; c <= WM; c++) xw[c] = czero();
@@ -328,31 +327,62 @@ PSB_HD double sweep_s4(const Shape& s, LV F, LV T, LV RA, double scale) {
   return acc;
 }
 
-// Largest eigenvalue of the Lanczos tridiagonal T_k (alpha = hist[i].x, beta = hist[i].y),
-// by Newton on det(T_k - x I) from an upper bound x0 (monotone from the right, since all
-// roots are real). Returns theta; *s2 = square of the last component of its eigenvector
-// (= -1 / d_k'(theta) in the LDL^T pivot recurrence), used for the Ritz residual beta_k |s_k|.
-PSB_HD double ritz_top(const double2* hist, int ld, int k, double x0, double* s2) {
-  double x = x0, dp = -1.0;
-  for (int it = 0; it < 200; it++) {
-    double2 h0 = hist[0];
-    double d = h0.x - x;
-    dp = -1.0;
-    double q = 1.0 / d;
-    double S = dp * q;
-    for (int j = 1; j < k; j++) {
-      const double bj = hist[(int64_t)(j - 1) * ld].y;
-      const double b2 = bj * bj;
+// Largest eigenvalue of the Lanczos tridiagonal T_k (alpha = hist[i].x, beta = hist[i].y).
+// Newton on det(T_k - x I) via the LDL^T pivot recurrence d_j(x), started from the interlacing
+// bound x0 = top eigenvalue of [[theta_{k-1}, beta_{k-1} s_{k-1}], [., alpha_k]] (s_{k-1}: last
+// component of T_{k-1}'s top Ritz vector), which lies between the two largest roots of T_k, so
+// Newton converges to the largest one (quadratically once close; a near-double root from a
+// ghost only slows it to linear). Guarded by the Weyl upper bound xu. Returns theta;
+// *s2 = square of the last component of its eigenvector (= -1 / d_k'(theta)), used for the
+// Ritz residual beta_k |s_k|.
+PSB_HD double ritz_eval(const double2* hist, int ld, int k, double x, double* dp_out) {
+  double d = hist[0].x - x, dp = -1.0;
+  double q = 1.0 / d;
+  double S = dp * q;
+  int j = 1;
+  for (; j + 3 < k; j += 4) {  // 4 independent history loads in flight
+    const double2 h0 = hist[(int64_t)(j - 1) * ld], h1 = hist[(int64_t)j * ld];
+    const double2 h2 = hist[(int64_t)(j + 1) * ld], h3 = hist[(int64_t)(j + 2) * ld];
+    const double2 h4 = hist[(int64_t)(j + 3) * ld];
+    const double a[4] = {h1.x, h2.x, h3.x, h4.x}, b[4] = {h0.y, h1.y, h2.y, h3.y};
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const double b2 = b[u] * b[u];
       const double dpn = fma(b2 * dp, q * q, -1.0);
-      d = hist[(int64_t)j * ld].x - x - b2 * q;
+      d = a[u] - x - b2 * q;
       q = 1.0 / d;
       dp = dpn;
       S = fma(dp, q, S);
     }
-    const double step = 1.0 / S;
-    if (!(step > 1e-15 * fabs(x))) break;
+  }
+  for (; j < k; j++) {
+    const double bj = hist[(int64_t)(j - 1) * ld].y;
+    const double b2 = bj * bj;
+    const double dpn = fma(b2 * dp, q * q, -1.0);
+    d = hist[(int64_t)j * ld].x - x - b2 * q;
+    q = 1.0 / d;
+    dp = dpn;
+    S = fma(dp, q, S);
+  }
+  *dp_out = dp;
+  return 1.0 / S;  // Newton step f/f'
+}
+
+PSB_HD double ritz_top(const double2* hist, int ld, int k, double theta_prev, double alpha, double beta,
+                       double* s2) {
+  // Upper bound: with f(x) = alpha - x + beta^2 sum_i s_i^2 / (x - theta_i) (secular function of
+  // T_k over T_{k-1}'s Ritz pairs, sum s_i^2 = 1) and x - theta_i >= x - theta_1, f(x) <=
+  // alpha - x + beta^2 / (x - theta_1), whose root is the top eigenvalue of
+  // [[theta_1, beta], [beta, alpha]]; Newton from there decreases monotonically to theta_k.
+  const double dm = 0.5 * (theta_prev - alpha);
+  double x = (0.5 * (theta_prev + alpha) + sqrt(dm * dm + beta * beta)) * (1.0 + 1e-14) + 1e-300;
+  double dp = -1.0;
+  for (int it = 0; it < 200; it++) {
+    const double step = ritz_eval(hist, ld, k, x, &dp);
+    if (!(step > 1e-15 * x)) break;
     x -= step;
   }
+  ritz_eval(hist, ld, k, x, &dp);
   *s2 = -1.0 / dp;
   return x;
 }

@@ -44,8 +44,8 @@ struct DevBuf {
 struct psb_handle {
   int device = 0;
   int num_sms = 148;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t stream = nullptr, stream2 = nullptr;
+  cudaEvent_t ev[8] = {};
   std::string err;
   std::mutex mu;
   // matrix
@@ -54,8 +54,8 @@ struct psb_handle {
   bool have_matrix = false;
   DevBuf Ab, AHA, v1;
   // per call
-  DevBuf zs, outidx, out, iters, status, listA, counters, scratch, pivs, dynL, dynD;
-  DevBuf xs, ys;
+  DevBuf zs, outidx, out, iters, status, listA, listB, counters, scratch, pivs, dynL, dynD;
+  DevBuf xs, ys, prof;
   // predictor
   DevBuf params, feat, eig, prob, region, idx;
   psb_stats stats{};
@@ -79,11 +79,21 @@ static int fail(psb_handle* h, int code, const std::string& msg) {
 // runtime-shape (DYN) instantiation.
 typedef void (*bis_fn)(BisArgs);
 typedef void (*lan_fn)(LanArgs);
-struct KPair { int kl, ku; bis_fn b; lan_fn l; };
-#define KP(KL, KU) {KL, KU, &k_bisect<KL, KU, false>, &k_lanczos<KL, KU, false>}
+struct KPair { int kl, ku; bis_fn b; lan_fn l; int lsmem; };
+constexpr int kDepth = 8;  // cp.async ring depth of the Lanczos sweeps (rows in flight + 1)
+#define KP(KL, KU) {KL, KU, &k_bisect<KL, KU, false>, &k_lanczos<KL, KU, false, kDepth>, 4 * Ring<KL, KU, kDepth>::BYTES}
 static const KPair kTable[] = {KP(1, 1), KP(1, 3), KP(2, 2), KP(2, 3), KP(3, 3), KP(4, 4), KP(1, 2), KP(2, 1)};
-static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true>, &k_lanczos<16, 16, true>};
+static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true>, &k_lanczos<16, 16, true, 2>, 0};
+static const KPair kExp[] = {{1, 1, &k_bisect<1, 1, false>, &k_lanczos<1, 1, false, 2>, 4 * Ring<1, 1, 2>::BYTES},
+                             {1, 1, &k_bisect<1, 1, false>, &k_lanczos<1, 1, false, 4>, 4 * Ring<1, 1, 4>::BYTES},
+                             {1, 1, &k_bisect<1, 1, false>, &k_lanczos<1, 1, false, 16>, 4 * Ring<1, 1, 16>::BYTES}};
 static KPair pick(int kl, int ku) {
+  if (kl == 1 && ku == 1 && getenv("PSB_DEPTH")) {  // development experiment: ring depth
+    const int d = atoi(getenv("PSB_DEPTH"));
+    if (d == 2) return kExp[0];
+    if (d == 4) return kExp[1];
+    if (d == 16) return kExp[2];
+  }
   for (const KPair& k : kTable)
     if (k.kl == kl && k.ku == ku) return k;
   return kDyn;
@@ -106,7 +116,8 @@ int psb_create(int device, psb_handle** out) {
   h->device = device;
   if (cudaSetDevice(device) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
   *out = h;
   return PSB_OK;
@@ -115,12 +126,13 @@ int psb_create(int device, psb_handle** out) {
 void psb_destroy(psb_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->v1, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA,
+  DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->v1, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
                     &h->counters, &h->scratch, &h->pivs, &h->dynL, &h->dynD, &h->xs, &h->ys, &h->params,
                     &h->feat, &h->eig, &h->prob, &h->region, &h->idx};
   for (DevBuf* b : bufs) b->release();
   for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
   if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->stream2) cudaStreamDestroy(h->stream2);
   delete h;
 }
 
@@ -211,10 +223,10 @@ static double flops_it_row(int kl, int ku) {
   return (4 + 3 + 8.0 * W + 6) + (8.0 * kl) + (8.0 * kl + 2) + (8.0 * W + 6 + 2 + 2);
 }
 static double bytes_it_row(int kl, int ku) {
-  const int W = kl + ku, NF = W + 1 + kl;
-  // factors read twice per step (S1,S4: U' + rinv; S2,S3: L) + pivots twice;
+  const int W = kl + ku;
+  // factors read twice per step (S1,S4: U' + rinv; S2,S3: L) + int32 pivots twice;
   // vectors: S1 r3 w3, S2 r1 w1, S3 r1 w1, S4 r2 w1
-  return 16.0 * (2.0 * (W + 1) + 2.0 * kl) + 2.0 + 16.0 * (6 + 2 + 2 + 3) + 0.0 * NF;
+  return 16.0 * (2.0 * (W + 1) + 2.0 * kl) + 8.0 + 16.0 * (6 + 2 + 2 + 3);
 }
 
 // Core pipeline on device buffers. zs/outidx/out/iters/status are device pointers.
@@ -239,15 +251,14 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
 
   CK(h->counters.ensure(sizeof(unsigned long long) * 8));
   CK(h->listA.ensure(sizeof(int64_t) * P));
+  CK(h->listB.ensure(sizeof(int64_t) * P));
   unsigned long long* cnt = h->counters.as<unsigned long long>();
   CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 8, st));
 
-  // ---- engine B (classification + bisection)
+  // ---- classification: one LDL^H test per point at lambda = (tau S)^2 splits the points
   int occB = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, kp.b, 128, 0));
   occB = std::max(occB, 1);
-  int64_t gridB = std::min<int64_t>((int64_t)occB * h->num_sms, (P + 127) / 128);
-  gridB = std::max<int64_t>(gridB, 1);
   BisArgs ba;
   ba.n = n; ba.kl = kl; ba.ku = ku;
   ba.Ab = h->Ab.as<double2>(); ba.AHA = h->AHA.as<double2>();
@@ -255,60 +266,103 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.anorm = h->anorm; ba.tau = opt.tau; ba.rtol = opt.bis_rtol;
   ba.force = opt.force_engine; ba.max_tests = 400;
   ba.out = d_out; ba.iters = d_iters; ba.status = d_status;
-  ba.listA = h->listA.as<int64_t>(); ba.counters = cnt;
+  ba.listA = h->listA.as<int64_t>(); ba.listB = h->listB.as<int64_t>(); ba.counters = cnt;
   ba.dyn_L = nullptr; ba.dyn_D = nullptr;
+  ba.mode = 0;
+  const int64_t gridC = std::max<int64_t>(1, std::min<int64_t>((int64_t)occB * h->num_sms, (P + 127) / 128));
+  int64_t gridB = (int64_t)occB * h->num_sms;
   if (dyn) {
     const int b = std::max(kl + ku, 1);
-    const int64_t threads = gridB * 128;
+    const int64_t threads = std::max(gridB, gridC) * 128;
     CK(h->dynL.ensure(sizeof(double2) * threads * b * b));
     CK(h->dynD.ensure(sizeof(double) * threads * 2 * b));
     ba.dyn_L = h->dynL.as<double2>(); ba.dyn_D = h->dynD.as<double>();
   }
   CK(cudaEventRecord(h->ev[0], st));
-  kp.b<<<(unsigned)gridB, 128, 0, st>>>(ba);
+  kp.b<<<(unsigned)gridC, 128, 0, st>>>(ba);
   CK(cudaGetLastError());
   CK(cudaEventRecord(h->ev[1], st));
+  unsigned long long hc0[8];
+  CK(cudaMemcpyAsync(hc0, cnt, sizeof(hc0), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int64_t nA = (int64_t)hc0[1], nB = (int64_t)hc0[7];
+  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));  // reset the work counter
 
-  // ---- engine L (band LU + inverse Lanczos) on the points engine B handed over
+  // ---- engine L (band LU + inverse Lanczos) on stream2, concurrently with engine B
   const Shape s = make_shape(n, kl, ku);
-  const int64_t warp_stride = ((int64_t)n * (s.NF + 3) + kmax) * 32;  // double2 units
-  const int64_t piv_stride = ((int64_t)n * 32 + 255) / 256 * 256;
+  const int64_t warp_stride = ((int64_t)n * (s.NU + s.NL + 3) + kmax) * 32;  // double2 units
+  const int64_t piv_stride = ((int64_t)n * 32 + 63) / 64 * 64;                 // int32 units
+  int64_t gridL = 0;
   int occL = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occL, kp.l, 128, 0));
-  occL = std::max(occL, 1);
-  const double budget = 24.0 * (1ull << 30);  // scratch budget (HBM is 180 GB)
-  int64_t warps = std::min<int64_t>((int64_t)occL * h->num_sms * 4, (P + 31) / 32);
-  const double per_warp = warp_stride * 16.0 + piv_stride;
-  warps = std::min<int64_t>(warps, (int64_t)(budget / per_warp));
-  warps = std::max<int64_t>(4, (warps + 3) / 4 * 4);
-  const int64_t gridL = warps / 4;
-  CK(h->scratch.ensure((size_t)(warps * warp_stride * sizeof(double2))));
-  CK(h->pivs.ensure((size_t)(warps * piv_stride)));
-  LanArgs la;
-  la.s = s; la.Ab = h->Ab.as<double2>(); la.v1 = h->v1.as<double2>();
-  la.zs = d_zs; la.outidx = d_outidx; la.listA = h->listA.as<int64_t>(); la.counters = cnt;
-  la.out = d_out; la.iters = d_iters; la.status = d_status;
-  la.scratch = h->scratch.as<double2>(); la.pivs = h->pivs.as<uint8_t>();
-  la.warp_stride = warp_stride; la.piv_stride = piv_stride;
-  la.kmax = kmax; la.refill = std::min(32, std::max(1, opt.refill));
-  kp.l<<<(unsigned)gridL, 128, 0, st>>>(la);
-  CK(cudaGetLastError());
+  if (nA > 0) {
+    if (kp.lsmem > 48 * 1024) CK(cudaFuncSetAttribute(kp.l, cudaFuncAttributeMaxDynamicSharedMemorySize, kp.lsmem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occL, kp.l, 128, kp.lsmem));
+    occL = std::max(occL, 1);
+    const double budget = 24.0 * (1ull << 30);  // scratch budget (HBM is 180 GB)
+    const double per_warp = warp_stride * 16.0 + piv_stride * 4.0;
+    int64_t warps = std::min<int64_t>((int64_t)occL * h->num_sms * 4, (nA + 31) / 32);
+    warps = std::min<int64_t>(warps, (int64_t)(budget / per_warp));
+    if (getenv("PSB_LWARPS")) warps = std::min<int64_t>(warps, atoll(getenv("PSB_LWARPS")));
+    warps = std::max<int64_t>(4, (warps + 3) / 4 * 4);
+    gridL = warps / 4;
+    CK(h->scratch.ensure((size_t)(warps * warp_stride * sizeof(double2))));
+    CK(h->pivs.ensure((size_t)(warps * piv_stride * 4)));
+    LanArgs la;
+    la.s = s; la.Ab = h->Ab.as<double2>(); la.v1 = h->v1.as<double2>();
+    la.zs = d_zs; la.outidx = d_outidx; la.listA = h->listA.as<int64_t>(); la.counters = cnt;
+    la.out = d_out; la.iters = d_iters; la.status = d_status;
+    la.scratch = h->scratch.as<double2>(); la.pivs = h->pivs.as<int>();
+    la.warp_stride = warp_stride; la.piv_stride = piv_stride;
+    la.kmax = kmax; la.refill = std::min(32, std::max(1, opt.refill));
+    la.prof = nullptr;
+    if (getenv("PSB_PROF")) {
+      CK(h->prof.ensure(64));
+      CK(cudaMemsetAsync(h->prof.p, 0, 64, st));
+      la.prof = h->prof.as<unsigned long long>();
+    }
+    CK(cudaEventRecord(h->ev[5], st));
+    CK(cudaStreamWaitEvent(h->stream2, h->ev[5], 0));
+    kp.l<<<(unsigned)gridL, 128, kp.lsmem, h->stream2>>>(la);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(h->ev[3], h->stream2));
+  }
+  // ---- engine B (bisection) on the caller's stream, sharing the SMs with engine L
+  if (nB > 0) {
+    int occShare = occB;
+    if (nA > 0 && occB > 1) occShare = occB - 1;  // leave room for one engine-L block per SM
+    gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, (nB + 127) / 128));
+    ba.mode = 1;
+    kp.b<<<(unsigned)gridB, 128, 0, st>>>(ba);
+    CK(cudaGetLastError());
+  } else {
+    gridB = 0;
+  }
   CK(cudaEventRecord(h->ev[2], st));
+  if (nA > 0) CK(cudaStreamWaitEvent(st, h->ev[3], 0));
+  CK(cudaEventRecord(h->ev[4], st));
   unsigned long long hc[8];
   CK(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  float msB = 0, msL = 0;
-  cudaEventElapsedTime(&msB, h->ev[0], h->ev[1]);
-  cudaEventElapsedTime(&msL, h->ev[1], h->ev[2]);
+  float msC = 0, msB = 0, msL = 0, msT = 0;
+  cudaEventElapsedTime(&msC, h->ev[0], h->ev[1]);
+  cudaEventElapsedTime(&msB, h->ev[1], h->ev[2]);
+  if (nA > 0) cudaEventElapsedTime(&msL, h->ev[1], h->ev[3]);
+  cudaEventElapsedTime(&msT, h->ev[0], h->ev[4]);
+  if (getenv("PSB_PROF") && nA > 0) {
+    unsigned long long pr[8];
+    cudaMemcpy(pr, h->prof.p, 64, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[psb prof] warp-cycles: lu %.3g s1 %.3g s2 %.3g s3 %.3g s4 %.3g ritz %.3g (gridL %lld)\n",
+            (double)pr[0], (double)pr[1], (double)pr[2], (double)pr[3], (double)pr[4], (double)pr[5], (long long)gridL);
+  }
   psb_stats& S = h->stats;
   S.n_bisect = (int64_t)hc[3];
   S.n_lanczos = (int64_t)hc[6];
-  S.pd_tests = (int64_t)hc[2];
+  S.pd_tests = (int64_t)hc[2] + nA;  // bisected points count their classification test; + Lanczos points' one
   S.lanczos_iters = (int64_t)hc[5];
-  S.flops_bisect = (double)hc[2] * n * flops_pd_row(kl, ku);
+  S.flops_bisect = (double)S.pd_tests * n * flops_pd_row(kl, ku);
   S.flops_lanczos = (double)hc[6] * n * flops_lu_row(kl, ku) + (double)hc[5] * n * flops_it_row(kl, ku);
-  S.bytes_lanczos = (double)hc[6] * n * 16.0 * (s.NF) + (double)hc[5] * n * bytes_it_row(kl, ku);
-  S.ms_bisect = msB; S.ms_lanczos = msL; S.ms_total = msB + msL;
+  S.bytes_lanczos = (double)hc[6] * n * (16.0 * (s.NU + kl) + 4.0) + (double)hc[5] * n * bytes_it_row(kl, ku);
+  S.ms_bisect = msC + msB; S.ms_lanczos = msL; S.ms_total = msT;
   S.grid_bisect = (int32_t)gridB; S.grid_lanczos = (int32_t)gridL;
   if ((int64_t)(hc[3] + hc[6]) != P)
     return fail(h, PSB_ERR_CUDA, "internal: points finished " + std::to_string(hc[3] + hc[6]) + " != " +

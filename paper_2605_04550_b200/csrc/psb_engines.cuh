@@ -23,7 +23,9 @@ struct BisArgs {
   int32_t* iters;
   int8_t* status;
   int64_t* listA;                 // points handed to the Lanczos engine
-  unsigned long long* counters;   // [0] work, [1] nA, [2] pd tests, [3] nB
+  int64_t* listB;                 // points the bisection engine owns (mode 1 input)
+  unsigned long long* counters;   // [0] work, [1] nA, [2] pd tests, [3] nB done, [7] nB listed
+  int mode;                       // 0: classify (one test, split into listA/listB); 1: bisect listB
   double2* dyn_L;                 // DYN only: per-thread b*b ring
   double* dyn_D;                  // DYN only: per-thread 2b
 };
@@ -39,11 +41,217 @@ struct LanArgs {
   double* out;
   int32_t* iters;
   int8_t* status;
-  double2* scratch;               // per warp: F n*NF*32 | T n*32 | RA n*32 | RB n*32 | hist kmax*32
-  uint8_t* pivs;                  // per warp: n*32
+  double2* scratch;               // per warp: FU n*NU*32 | FL n*NL*32 | T | RA | RB (n*32 each) | hist kmax*32
+  int* pivs;                      // per warp: n*32 int32
   int64_t warp_stride, piv_stride;
   int kmax, refill;
+  unsigned long long* prof;       // optional: per-phase clock64 totals [lu, s1, s2, s3, s4, ritz, idle]
 };
+
+// ---------------------------------------------------------------- cp.async row ring
+// Each lane streams only its own column (its own grid point), so a lane's cp.async groups
+// and waits are private: no warp barrier, no cross-lane hazard. Row j of a sweep lives in
+// ring slot (sweep step) % D; the copy for step q+D-1 is issued before waiting for step q.
+__device__ __forceinline__ void cp16(void* s, const void* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp4(void* s, const void* g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int KL, int KU, int D>
+struct Ring {
+  static constexpr int W = KL + KU, NU = W + 1, NL = (KL > 0 ? KL : 1), SF = W + 4;
+  static constexpr int BYTES = D * SF * 32 * 16 + D * 32 * 4;  // per warp
+  double2* d;  // this warp's ring
+  int* pv;     // pivot ring
+  int lane;
+  __device__ double2* at(int slot, int f) const { return d + ((slot * SF + f) << 5) + lane; }
+  __device__ int* pat(int slot) const { return pv + (slot << 5) + lane; }
+};
+
+// S1 (forward): r_k update and t = U^{-H} r_k, right-looking so row j's U' entries are consumed
+// at step j (the ring holds current/future rows only). Slot j: FU_j | T_j RA_j RB_j.
+template <int KL, int KU, int D>
+__device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV RB,
+                        const double2* __restrict__ v1, int k, double c1, double c2) {
+  typedef Ring<KL, KU, D> RG;
+  constexpr int W = RG::W, NU = RG::NU;
+  auto issue = [&](int j) {
+    if (j < n) {
+      const int sl = j % D;
+#pragma unroll
+      for (int f = 0; f < NU; f++) cp16(R.at(sl, f), FU.p + ((int64_t)j * NU + f) * 32);
+      if (k >= 2) {
+        cp16(R.at(sl, NU), T.p + (int64_t)j * 32);
+        cp16(R.at(sl, NU + 1), RA.p + (int64_t)j * 32);
+        if (k >= 3) cp16(R.at(sl, NU + 2), RB.p + (int64_t)j * 32);
+      }
+    }
+    cp_commit();
+  };
+  double2 acc[W + 1];
+#pragma unroll
+  for (int d = 0; d <= W; d++) acc[d] = czero();
+  double bsq = 0.0;
+#pragma unroll
+  for (int q = 0; q < D - 1; q++) issue(q);
+  for (int j = 0; j < n; j++) {
+    issue(j + D - 1);
+    cp_wait<D - 1>();
+    const int sl = j % D;
+    double2 r;
+    if (k == 1) {
+      r = v1[j];
+      RA.put(j, r);
+    } else {
+      const double2 ra = *R.at(sl, NU + 1);
+      r = cfms_r(*R.at(sl, NU), c1, ra);
+      if (k >= 3) r = cfms_r(r, c2, *R.at(sl, NU + 2));
+      RB.put(j, ra);
+      RA.put(j, r);
+      bsq += cnorm2(r);
+    }
+    const double2 tp = cadd(r, acc[0]);
+    T.put(j, cmul(tp, cconj(*R.at(sl, W))));
+#pragma unroll
+    for (int d = 1; d <= W; d++) acc[d - 1] = cfms_cj(acc[d], *R.at(sl, d - 1), tp);
+    acc[W] = czero();
+  }
+  cp_wait<0>();
+  return bsq;
+}
+
+// S2 (backward): E^H. Slot (step q, row j = n-1-q): FL_j | T_j, piv_j. Returns ||out||^2.
+template <int KL, int KU, int D>
+__device__ double pl_s2(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T) {
+  typedef Ring<KL, KU, D> RG;
+  constexpr int NL = RG::NL;
+  auto issue = [&](int q) {
+    const int j = n - 1 - q;
+    if (j >= 0) {
+      const int sl = q % D;
+#pragma unroll
+      for (int f = 0; f < KL; f++) cp16(R.at(sl, f), FL.p + ((int64_t)j * NL + f) * 32);
+      cp16(R.at(sl, NL), T.p + (int64_t)j * 32);
+      cp4(R.pat(sl), piv.p + (int64_t)j * 32);
+    }
+    cp_commit();
+  };
+  double2 yw[KL + 1];
+#pragma unroll
+  for (int r = 0; r <= KL; r++) yw[r] = czero();
+  double nrm = 0.0;
+#pragma unroll
+  for (int q = 0; q < D - 1; q++) issue(q);
+  for (int q = 0; q < n; q++) {
+    const int j = n - 1 - q;
+    issue(q + D - 1);
+    cp_wait<D - 1>();
+    const int sl = q % D;
+    const int out = j + 1 + KL;
+    if (out < n) { T.put(out, yw[KL]); nrm += cnorm2(yw[KL]); }
+#pragma unroll
+    for (int r = KL; r >= 1; r--) yw[r] = yw[r - 1];
+    double2 y = *R.at(sl, NL);
+#pragma unroll
+    for (int r = KL; r >= 1; r--) y = cfms_cj(y, *R.at(sl, r - 1), yw[r]);
+    yw[0] = y;
+    const int p = *R.pat(sl);
+#pragma unroll
+    for (int r = 1; r <= KL; r++)
+      if (p == r) { const double2 t = yw[0]; yw[0] = yw[r]; yw[r] = t; }
+  }
+  cp_wait<0>();
+#pragma unroll
+  for (int r = 0; r <= KL; r++)
+    if (r < n) { T.put(r, yw[r]); nrm += cnorm2(yw[r]); }
+  return nrm;
+}
+
+// S3 (forward): E applied to scale*T in place. Slot j: FL_j | T_{j+1+KL}, piv_j.
+template <int KL, int KU, int D>
+__device__ void pl_s3(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T, double scale) {
+  typedef Ring<KL, KU, D> RG;
+  constexpr int NL = RG::NL;
+  auto issue = [&](int j) {
+    if (j < n) {
+      const int sl = j % D;
+#pragma unroll
+      for (int f = 0; f < KL; f++) cp16(R.at(sl, f), FL.p + ((int64_t)j * NL + f) * 32);
+      if (j + 1 + KL < n) cp16(R.at(sl, NL), T.p + (int64_t)(j + 1 + KL) * 32);
+      cp4(R.pat(sl), piv.p + (int64_t)j * 32);
+    }
+    cp_commit();
+  };
+  double2 bw[KL + 1];
+#pragma unroll
+  for (int r = 0; r <= KL; r++) bw[r] = (r < n) ? cscale(T.get(r), scale) : czero();
+#pragma unroll
+  for (int q = 0; q < D - 1; q++) issue(q);
+  for (int j = 0; j < n; j++) {
+    issue(j + D - 1);
+    cp_wait<D - 1>();
+    const int sl = j % D;
+    const int p = *R.pat(sl);
+#pragma unroll
+    for (int r = 1; r <= KL; r++)
+      if (p == r) { const double2 t = bw[0]; bw[0] = bw[r]; bw[r] = t; }
+#pragma unroll
+    for (int r = 1; r <= KL; r++) bw[r] = cfms(bw[r], *R.at(sl, r - 1), bw[0]);
+    T.put(j, bw[0]);
+#pragma unroll
+    for (int r = 0; r < KL; r++) bw[r] = bw[r + 1];
+    bw[KL] = (j + 1 + KL < n) ? cscale(*R.at(sl, NL), scale) : czero();
+  }
+  cp_wait<0>();
+}
+
+// S4 (backward): x = U^{-1}(scale*T) in place; returns sum Re(conj(RA_j) x_j).
+// Slot (step q, row j = n-1-q): FU_j | T_j RA_j.
+template <int KL, int KU, int D>
+__device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, double scale) {
+  typedef Ring<KL, KU, D> RG;
+  constexpr int W = RG::W, NU = RG::NU;
+  auto issue = [&](int q) {
+    const int j = n - 1 - q;
+    if (j >= 0) {
+      const int sl = q % D;
+#pragma unroll
+      for (int f = 0; f < NU; f++) cp16(R.at(sl, f), FU.p + ((int64_t)j * NU + f) * 32);
+      cp16(R.at(sl, NU), T.p + (int64_t)j * 32);
+      cp16(R.at(sl, NU + 1), RA.p + (int64_t)j * 32);
+    }
+    cp_commit();
+  };
+  double2 xw[W + 1];
+#pragma unroll
+  for (int c = 0; c <= W; c++) xw[c] = czero();
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < D - 1; q++) issue(q);
+  for (int q = 0; q < n; q++) {
+    const int j = n - 1 - q;
+    issue(q + D - 1);
+    cp_wait<D - 1>();
+    const int sl = q % D;
+    double2 x = cmul(cscale(*R.at(sl, NU), scale), *R.at(sl, W));
+#pragma unroll
+    for (int c = W; c >= 1; c--) x = cfms(x, *R.at(sl, c - 1), xw[c]);
+    T.put(j, x);
+    acc += cdotr(*R.at(sl, NU + 1), x);
+#pragma unroll
+    for (int c = W; c >= 2; c--) xw[c] = xw[c - 1];
+    xw[1] = x;
+  }
+  cp_wait<0>();
+  return acc;
+}
 
 __device__ __forceinline__ int64_t out_index(const int64_t* outidx, int64_t p) { return outidx ? outidx[p] : p; }
 
@@ -59,6 +267,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   BisState st;
   st.lam = 1.0; st.tests = 0; st.phase = 0; st.lo = st.hi = 0.0;
   bool exhausted = false;
+  const int64_t total = (a.mode == 0) ? a.P : (int64_t)a.counters[7];
   while (true) {
     unsigned idle = __ballot_sync(FULL, p < 0);
     if (idle && !exhausted) {
@@ -69,18 +278,22 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       if (p < 0) {
         const int rank = __popc(idle & ((1u << lane) - 1u));
         const int64_t q = (int64_t)base + rank;
-        if (q < a.P) {
-          z = a.zs[q];
-          if (a.force == 1) {  // Lanczos-only mode: hand over immediately
+        if (q < total) {
+          const int64_t pt = (a.mode == 0) ? q : a.listB[q];
+          z = a.zs[pt];
+          if (a.mode == 0 && a.force == 1) {  // Lanczos-only mode: hand over immediately
             unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
-            a.listA[slot] = q;
+            a.listA[slot] = pt;
           } else {
-            p = q;
+            p = pt;
             bis_start(st, hypot(z.x, z.y), a.anorm, a.tau);
+            if (a.mode == 1) {  // classification test already passed: lambda_tau is PD
+              st.tests = 1; st.phase = 1; st.lo = st.lam; st.hi = 4.0 * st.lam; st.lam = st.hi;
+            }
           }
         }
       }
-      if ((int64_t)base + cnt >= a.P) exhausted = true;
+      if ((int64_t)base + cnt >= total) exhausted = true;
     }
     const unsigned act = __ballot_sync(FULL, p >= 0);
     if (!act) {
@@ -105,7 +318,18 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         if ((++grp & 7) == 0 && !__any_sync(FULL, pd && me)) break;  // every active lane failed
       }
     }
-    if (me) {
+    if (me && a.mode == 0) {
+      // classification only: PD at (tau S)^2 -> bisection list; else Lanczos list
+      if (pd || a.force == 2) {
+        unsigned long long slot = atomicAdd(&a.counters[7], 1ull);
+        a.listB[slot] = p;
+      } else {
+        unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
+        a.listA[slot] = p;
+      }
+      p = -1;
+    }
+    if (me && a.mode == 1) {
       const int r = bis_update(st, pd, a.rtol, a.force == 2, a.max_tests);
       if (r == BIS_DONE || r == BIS_FAIL) {
         const int64_t o = out_index(a.outidx, p);
@@ -126,7 +350,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
 }
 
 // ----------------------------------------------------------------- engine L kernel
-template <int KL, int KU, bool DYN>
+template <int KL, int KU, bool DYN, int DPIPE>
 __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -134,12 +358,23 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
   const Shape s = a.s;
   const int n = s.n;
   double2* base = a.scratch + gw * a.warp_stride;
-  const LV F{base + lane, 32};
-  const LV T{base + (int64_t)n * s.NF * 32 + lane, 32};
-  const LV RA{base + (int64_t)n * (s.NF + 1) * 32 + lane, 32};
-  const LV RB{base + (int64_t)n * (s.NF + 2) * 32 + lane, 32};
-  double2* hist = base + (int64_t)n * (s.NF + 3) * 32 + lane;
+  const LV FU{base + lane, 32};
+  const LV FL{base + (int64_t)n * s.NU * 32 + lane, 32};
+  const int64_t vo = (int64_t)n * (s.NU + s.NL) * 32;
+  const LV T{base + vo + lane, 32};
+  const LV RA{base + vo + (int64_t)n * 32 + lane, 32};
+  const LV RB{base + vo + (int64_t)n * 64 + lane, 32};
+  double2* hist = base + vo + (int64_t)n * 96 + lane;
   const LVb piv{a.pivs + gw * a.piv_stride + lane, 32};
+  typedef Ring<(KL > 0 ? KL : 1), KU, DPIPE> RG;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RG ring;
+  if constexpr (!DYN) {
+    const int wib = threadIdx.x >> 5;
+    ring.d = reinterpret_cast<double2*>(smem_raw + (size_t)wib * RG::BYTES);
+    ring.pv = reinterpret_cast<int*>(smem_raw + (size_t)wib * RG::BYTES + DPIPE * RG::SF * 32 * 16);
+    ring.lane = lane;
+  }
   const int64_t nA = (int64_t)a.counters[1];
 
   int64_t p = -1;
@@ -177,14 +412,17 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       }
       if ((int64_t)bq + nidle >= nA) exhausted = true;
     }
+    long long tq0 = clock64();
     if (phase == 1) {
-      const bool ok = lu_factor<KL, KU, DYN>(s, a.Ab, z, F, piv);
+      const bool ok = lu_factor<KL, KU, DYN>(s, a.Ab, z, FU, FL, piv);
       if (!ok) {
         finish(0.0, 0, 2);
       } else {
         phase = 2; k = 1; nu = 1.0; b1 = 1.0; b2 = 1.0; aprev = 0.0; theta = 0.0; s2 = 1.0; dth = 0.0;
       }
     }
+    long long tq1 = clock64();
+    if (a.prof && lane == 0) atomicAdd(&a.prof[0], (unsigned long long)(tq1 - tq0));
     const unsigned act = __ballot_sync(FULL, phase == 2);
     if (!act) {
       if (exhausted && __ballot_sync(FULL, phase != 0) == 0) break;
@@ -194,7 +432,10 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       // S1: r_k and U^{-H} r_k
       const double c1 = (k >= 2) ? aprev / b1 : 0.0;
       const double c2 = (k >= 3) ? b1 / b2 : 0.0;
-      const double bsq = sweep_s1<KL, KU, DYN>(s, F, T, RA, RB, a.v1, k, c1, c2);
+      double bsq;
+      if constexpr (DYN) bsq = sweep_s1<KL, KU, DYN>(s, FU, T, RA, RB, a.v1, k, c1, c2);
+      else bsq = pl_s1<KL, KU, DPIPE>(n, ring, FU, T, RA, RB, a.v1, k, c1, c2);
+      if (a.prof) { long long t = clock64(); if (__activemask() && lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[1], (unsigned long long)(t - tq1)); tq1 = t; }
       if (k >= 2) {
         const double beta = sqrt(bsq);  // beta_{k-1}
         hist[(int64_t)(k - 2) * 32].y = beta;
@@ -213,24 +454,35 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
     }
     if (phase == 2) {
       // S2: E^H  (after S2: M^{-H} v_k * beta_{k-1})
-      const double nrm = sweep_s2<KL, KU, DYN>(s, F, piv, T);
+      double nrm;
+      if constexpr (DYN) nrm = sweep_s2<KL, KU, DYN>(s, FL, piv, T);
+      else nrm = pl_s2<KL, KU, DPIPE>(n, ring, FL, piv, T);
+      if (a.prof) { long long t = clock64(); if (lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[2], (unsigned long long)(t - tq1)); tq1 = t; }
       if (k == 1) {
         nu = sqrt(nrm);
         if (!(nu > 0.0) || !isfinite(nu)) finish(0.0, 0, 2);  // singular to working precision
       }
     }
     if (phase == 2) {
-      sweep_s3<KL, KU, DYN>(s, F, piv, T, 1.0 / (nu * b1));
-      const double acc = sweep_s4<KL, KU, DYN>(s, F, T, RA, 1.0 / nu);
+      double acc;
+      if constexpr (DYN) {
+        sweep_s3<KL, KU, DYN>(s, FL, piv, T, 1.0 / (nu * b1));
+        acc = sweep_s4<KL, KU, DYN>(s, FU, T, RA, 1.0 / nu);
+      } else {
+        pl_s3<KL, KU, DPIPE>(n, ring, FL, piv, T, 1.0 / (nu * b1));
+        if (a.prof) { long long t = clock64(); if (lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[3], (unsigned long long)(t - tq1)); tq1 = t; }
+        acc = pl_s4<KL, KU, DPIPE>(n, ring, FU, T, RA, 1.0 / nu);
+        if (a.prof) { long long t = clock64(); if (lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[4], (unsigned long long)(t - tq1)); tq1 = t; }
+      }
       const double alpha = acc / b1;
       hist[(int64_t)(k - 1) * 32] = cmk(alpha, 0.0);
       double th, sq;
       if (k == 1) {
         th = alpha; sq = 1.0;
       } else {
-        const double x0 = (fmax(theta, alpha) + b1) * (1.0 + 1e-14) + 1e-300;
-        th = ritz_top(hist, 32, k, x0, &sq);
+        th = ritz_top(hist, 32, k, theta, alpha, b1, &sq);
       }
+      if (a.prof) { long long t = clock64(); if (lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[5], (unsigned long long)(t - tq1)); tq1 = t; }
       dth = th - theta;
       theta = th;
       s2 = sq;

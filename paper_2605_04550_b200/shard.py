@@ -1,0 +1,74 @@
+"""K3 — grid partitioner across the GPUs of one box (replaces pseudospec/core.py:186-195, the
+ProcessPoolExecutor over row blocks).
+
+Points of the (compacted) row-major point list are dealt cyclically, point p -> rank p mod N:
+σ_min cost is spatially correlated (slow clusters outside the spectrum), so contiguous row
+blocks (core.py:189) would unbalance the ranks, while a cyclic deal spreads every region over
+all of them. Each rank evaluates its shard with its own device; the only exchange is the final
+gather of the σ map (NCCL all-gather over NVLink on GPUs; gloo in the CPU tests). Values are
+bitwise identical to the single-GPU map because every σ depends only on (A, z).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+
+
+def shard_indices(P: int, rank: int, world: int) -> np.ndarray:
+    """Indices of the points owned by `rank` under the cyclic deal."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world of size {world}")
+    return np.arange(rank, P, world, dtype=np.int64)
+
+
+def shard_count(P: int, rank: int, world: int) -> int:
+    return (P - rank + world - 1) // world if P > rank else 0
+
+
+def assemble(parts: list[np.ndarray], P: int) -> np.ndarray:
+    """Inverse of the cyclic deal: parts[r] holds the values of shard_indices(P, r, world)."""
+    world = len(parts)
+    out = np.empty(P, dtype=parts[0].dtype if parts else float)
+    for r, vals in enumerate(parts):
+        out[r::world] = vals
+    return out
+
+
+def gather_values(local: np.ndarray, P: int, group=None, device=None) -> np.ndarray:
+    """All-gather every rank's shard values (float64) and reassemble the full length-P array.
+
+    Shards differ in length by at most one; they are padded to the same length for the
+    collective. Works with the gloo (CPU tensors) and nccl (CUDA tensors) backends."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    m = (P + world - 1) // world
+    buf = torch.full((m,), float("nan"), dtype=torch.float64, device=device)
+    buf[: local.size] = torch.from_numpy(np.ascontiguousarray(local, dtype=np.float64)).to(buf.device)
+    out = torch.empty(world * m, dtype=torch.float64, device=device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    out = out.cpu().numpy().reshape(world, m)
+    parts = [out[r, : shard_count(P, r, world)] for r in range(world)]
+    return assemble(parts, P)
+
+
+def sharded_sigma(zs: np.ndarray, evaluate: Callable[[np.ndarray], np.ndarray], group=None,
+                  device=None) -> np.ndarray:
+    """σ at every z of zs on this process group: evaluate the local cyclic shard, all-gather."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    zs = np.asarray(zs, dtype=complex).ravel()
+    local = evaluate(zs[shard_indices(zs.size, rank, world)])
+    return gather_values(np.asarray(local, dtype=np.float64), zs.size, group=group, device=device)
+
+
+def sharded_full_pseudospectrum(A, grid, group=None, label: str = "matrix"):
+    """full_pseudospectrum (core.py:177-195) across the ranks of `group`, one GPU per rank."""
+    import torch
+    from . import core
+    dev = torch.device("cuda", torch.cuda.current_device())
+    vals = sharded_sigma(grid.points().ravel(), lambda z: core.smin_many(A, z, label=label),
+                         group=group, device=dev)
+    return core.SigmaField(grid, vals.reshape(grid.shape))

@@ -1,0 +1,170 @@
+"""K1 parity on the GPU (-m gpu): σ_min from libpsb200.so against the reference's zgesdd fixtures.
+
+Gate: |σ - σ_ref| <= 1e-9 * max(σ_ref, 1e-5 ||A||_2); ε-masks identical
+except where |σ_ref - ε| is inside that band; plus the reference's own test forms
+(tests/test_core.py:96-152, tests/test_acceptance.py:53-85,145-157 of the reference).
+"""
+
+import numpy as np
+import pytest
+
+from oracle.sigma_oracle import floored_rel_err
+from paper_2605_04550_b200 import _lib, configs, core
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def check(got, want, norm2, what):
+    floor = 1e-5 * norm2
+    e = floored_rel_err(got, want, floor)
+    assert np.all(np.isfinite(got)), what
+    assert e.max() <= TOL, f"{what}: worst floored rel err {e.max():.3e} at {int(np.argmax(e))}"
+    return e.max()
+
+
+def masks_agree(got, want, norm2, eps_levels):
+    band = TOL * np.maximum(want, 1e-5 * norm2)
+    for eps in eps_levels:
+        m_got, m_want = got <= eps, want <= eps
+        diff = m_got != m_want
+        assert not np.any(diff & (np.abs(want - eps) > band)), f"mask mismatch at eps={eps}"
+
+
+def test_c1_full_grid_and_eps_masks(gpu, gold):
+    z = gold("c1_full.npz")
+    cfg = configs.CONFIGS["C1"]
+    fld = core.full_pseudospectrum(cfg.matrix(), cfg.grid)
+    check(fld.values, z["values"], float(z["norm2"]), "C1")
+    masks_agree(fld.values, z["values"], float(z["norm2"]), [10.0 ** -k for k in range(1, 9)])
+    st = core.last_stats()
+    assert st["n_lanczos"] > 0 and st["n_bisect"] > 0 and st["n_lanczos"] + st["n_bisect"] == 2500
+
+
+def test_demo01_golden_including_exact_zeros(gpu, gold):
+    """demos/output_01_field.csv: nilpotent shift n=32, 120x120; 85 points with σ_ref = 0."""
+    want = gold("demo01_field.npz")["values"]
+    A = np.diag(np.ones(31), k=-1)
+    fld = core.full_pseudospectrum(A, core.make_grid(-1.5, 1.5, -1.5, 1.5, 120, 120))
+    check(fld.values, want, 1.0, "demo01")
+    masks_agree(fld.values, want, 1.0, [1e-2, 1e-4, 1e-8])
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_config_samples(gpu, gold, name):
+    z = gold(f"{name}_sample.npz")
+    cfg = configs.CONFIGS[name.upper()]
+    got = core.smin_many(cfg.matrix(), z["zs"])
+    check(got, z["sigma"], float(z["norm2"]), name)
+
+
+def test_c5_sample(gpu, gold):
+    z = gold("c5_sample.npz")
+    cfg = configs.CONFIGS["C5"]
+    for r, m in enumerate(z["matrices"]):
+        got = core.smin_many(cfg.matrix(int(m)), z["zs"][r])
+        check(got, z["sigma"][r], float(z["norm2"][r]), f"C5[{m}]")
+
+
+def test_small_random_reference_acceptance_form(gpu, gold):
+    """tests/test_acceptance.py:53-70: |got - want| / max(1, want) < 1e-10 over random banded A."""
+    z = gold("small_random.npz")
+    worst = 0.0
+    for t in range(len(z["A"])):
+        n = int(z["n"][t])
+        got = core.smin_many(z["A"][t][:n, :n], z["zs"][t])
+        worst = max(worst, float(np.max(np.abs(got - z["sigma"][t]) / np.maximum(1.0, z["sigma"][t]))))
+    assert worst < 1e-10
+
+
+def test_normality_identity(gpu):
+    """tests/test_acceptance.py:73-85: symmetric A -> σ_min = dist(z, spectrum) within 1e-8."""
+    rng = np.random.default_rng(20)
+    zs = core.make_grid(-3, 3, -3, 3, 10, 10).points().ravel()
+    worst = 0.0
+    for _ in range(5):
+        M = rng.standard_normal((12, 12))
+        A = (M + M.T) / 2
+        lam = np.linalg.eigvalsh(A)
+        d = np.abs(zs[:, None] - lam[None, :]).min(axis=1)
+        worst = max(worst, float(np.abs(core.smin_many(A, zs) - d).max()))
+    assert worst < 1e-8
+
+
+def test_identity_and_singular_shift(gpu):
+    g = core.make_grid(0, 2, -1, 1, 3, 3)
+    fld = core.full_pseudospectrum(np.eye(2), g)
+    assert np.allclose(fld.values, np.abs(g.points() - 1.0), atol=1e-12)
+    assert core.smin_at(np.diag(np.ones(3), -1), 0.0) == pytest.approx(0.0, abs=1e-15)
+    assert core.smin_at(np.eye(2), 3.0) == pytest.approx(2.0, abs=1e-12)
+
+
+def test_shift_covariance(gpu):
+    A = configs.grcar_band(40).todense().real
+    for c in (0.7, -1.3, 2.0):
+        z = 0.4 + 0.9j
+        assert abs(core.smin_at(A + c * np.eye(40), z + c) - core.smin_at(A, z)) < 1e-10
+
+
+def test_restricted_equals_full_bitwise(gpu):
+    cfg = configs.CONFIGS["C1"]
+    A = cfg.matrix()
+    full = core.full_pseudospectrum(A, cfg.grid)
+    rng = np.random.default_rng(5)
+    region = rng.uniform(size=cfg.grid.shape) < 0.2
+    res = core.restricted_field(A, cfg.grid, region)
+    assert np.array_equal(res.values[region], full.values[region])
+    assert np.all(np.isnan(res.values[~region]))
+    empty = core.restricted_field(A, cfg.grid, np.zeros(cfg.grid.shape, bool))
+    assert np.all(np.isnan(empty.values))
+
+
+def test_batch_order_and_pointwise_invariance_bitwise(gpu):
+    """Values depend only on (A, z): pointwise == batched, any order, any batch, any call."""
+    A = configs.CONFIGS["C2"].matrix()
+    zs = configs.CONFIGS["C2"].grid.points().ravel()[::97]
+    base = core.smin_many(A, zs)
+    perm = np.random.default_rng(1).permutation(zs.size)
+    assert np.array_equal(core.smin_many(A, zs[perm]), base[perm])
+    assert np.array_equal(core.smin_many(A, zs), base)
+    for i in range(0, zs.size, 50):
+        assert core.smin_at(A, zs[i]) == base[i]
+    parts = np.concatenate([core.smin_many(A, zs[i:i + 37]) for i in range(0, zs.size, 37)])
+    assert np.array_equal(parts, base)
+
+
+def test_engines_agree_where_both_apply(gpu):
+    """Forcing all points through either engine gives the same σ (points with σ >= tau*S)."""
+    A = configs.CONFIGS["C1"].matrix()
+    zs = configs.CONFIGS["C1"].grid.points().ravel()
+    auto, _, st = core.smin_many(A, zs, return_info=True)
+    sel = zs[st == 1][:300]
+    lan = core.smin_many(A, sel, opts=_lib.make_opts(force_engine=1))
+    bis = core.smin_many(A, sel, opts=_lib.make_opts(force_engine=2))
+    assert np.max(np.abs(lan - bis) / bis) < 1e-10
+
+
+def test_c2_full_grid_properties(gpu):
+    """Full-size (40,000-point) checks: all converged; σ is 1-Lipschitz in z; bounded by ||zI-A||."""
+    cfg = configs.CONFIGS["C2"]
+    A = cfg.matrix()
+    vals, iters, st = core.smin_many(A, cfg.grid.points().ravel(), return_info=True)
+    assert np.all(st <= 2)
+    v = vals.reshape(cfg.grid.shape)
+    dx = cfg.grid.xs()[1] - cfg.grid.xs()[0]
+    dy = cfg.grid.ys()[1] - cfg.grid.ys()[0]
+    assert np.all(np.abs(np.diff(v, axis=1)) <= dx * (1 + 1e-9) + 1e-12)
+    assert np.all(np.abs(np.diff(v, axis=0)) <= dy * (1 + 1e-9) + 1e-12)
+    assert np.all(v >= 0) and np.all(v <= np.abs(cfg.grid.points()) + 4.0)
+
+
+def test_edge_cases(gpu):
+    assert core.smin_many(np.eye(3), np.zeros(0, complex)).shape == (0,)
+    assert core.smin_at(np.array([[0.0, 1.0], [0.0, 0.0]]), 0.0) == 0.0
+    dense16 = np.random.default_rng(3).standard_normal((16, 16))  # kl = ku = 15 (runtime-shape kernels)
+    zs = np.array([0.3 + 0.1j, -2 + 1j, 5j])
+    from oracle.sigma_oracle import smin_restated
+    check(core.smin_many(dense16, zs), smin_restated(dense16, zs), np.linalg.norm(dense16, 2), "dense16")
+    diag = np.diag(np.arange(1.0, 6.0))  # kl = ku = 0
+    assert np.allclose(core.smin_many(diag, [2.5 + 0j, 10j]),
+                       [0.5, np.abs(10j - np.arange(1, 6)).min()], rtol=1e-12)
