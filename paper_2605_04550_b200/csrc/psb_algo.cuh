@@ -424,48 +424,67 @@ PSB_HD double2 g_entry(int n, int j, int d, const double2* __restrict__ Ab, cons
   return v;
 }
 
-// One row of the factorization for static shapes; U = j mod B (compile-time).
-template <int KLM, int KUM, int U>
-PSB_HD bool pd_row(PDRing<KLM, KUM>& R, int n, int j, const double2* __restrict__ Ab,
-                   const double2* __restrict__ AHA, double2 z, double zz) {
+// Reciprocal for the LDL^H pivots: MUFU seed + two Newton steps (~1 ulp; the PD decision only
+// needs the sign of every pivot, and L = s / D is insensitive to an ulp in 1/D).
+PSB_HD double fast_rcp(double x) {
+#ifdef __CUDA_ARCH__
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+
+// One row of the factorization for static shapes, for NP independent shifts lambda_q that share
+// the off-diagonal G entries (only the diagonal depends on lambda). U = j mod B (compile-time).
+template <int KLM, int KUM, int NP, int U>
+PSB_HD void pd_row(PDRing<KLM, KUM> (&R)[NP], int n, int j, const double2* __restrict__ Ab,
+                   const double2* __restrict__ AHA, double2 z, const double (&zz)[NP], bool (&pd)[NP]) {
   constexpr int B = KLM + KUM;
   double2 g[B + 1];
 #pragma unroll
-  for (int d = 0; d <= B; d++) g[d] = (j - d >= 0) ? g_entry<KLM, KUM>(n, j, d, Ab, AHA, z, zz) : czero();
-  double2 Lj[B + 1], LD[B + 1];
+  for (int d = 0; d <= B; d++) g[d] = (j - d >= 0) ? g_entry<KLM, KUM>(n, j, d, Ab, AHA, z, 0.0) : czero();
 #pragma unroll
-  for (int d = B; d >= 1; d--) {
-    constexpr int dummy = 0; (void)dummy;
-    const int sc = (U - d + 2 * B) % B;
-    double2 sacc = g[d];
+  for (int q = 0; q < NP; q++) {
+    double2 Lj[B + 1], LD[B + 1];
 #pragma unroll
-    for (int dm = B; dm > d; dm--) sacc = cfms_cj(sacc, R.L[sc][dm - d - 1], LD[dm]);
-    Lj[d] = cscale(sacc, R.iD[sc]);
-    LD[d] = cscale(Lj[d], R.D[sc]);
+    for (int d = B; d >= 1; d--) {
+      const int sc = (U - d + 2 * B) % B;
+      double2 sacc = g[d];
+#pragma unroll
+      for (int dm = B; dm > d; dm--) sacc = cfms_cj(sacc, R[q].L[sc][dm - d - 1], LD[dm]);
+      Lj[d] = cscale(sacc, R[q].iD[sc]);
+      LD[d] = cscale(Lj[d], R[q].D[sc]);
+    }
+    double dj = g[0].x + zz[q];
+#pragma unroll
+    for (int d = 1; d <= B; d++) dj -= cdotr(Lj[d], LD[d]);
+#pragma unroll
+    for (int d = 1; d <= B; d++) R[q].L[U][d - 1] = Lj[d];
+    R[q].D[U] = dj;
+    R[q].iD[U] = fast_rcp(dj);
+    pd[q] = pd[q] && (dj > 0.0);
   }
-  double dj = g[0].x;
-#pragma unroll
-  for (int d = 1; d <= B; d++) dj -= cdotr(Lj[d], LD[d]);
-#pragma unroll
-  for (int d = 1; d <= B; d++) R.L[U][d - 1] = Lj[d];
-  R.D[U] = dj;
-  R.iD[U] = 1.0 / dj;
-  return dj > 0.0;
 }
 
-template <int KLM, int KUM, int U>
+template <int KLM, int KUM, int NP, int U>
 struct PDUnroll {
-  PSB_HD static void run(PDRing<KLM, KUM>& R, int n, int jb, const double2* Ab, const double2* AHA, double2 z,
-                         double zz, bool& pd) {
+  PSB_HD static void run(PDRing<KLM, KUM> (&R)[NP], int n, int jb, const double2* Ab, const double2* AHA,
+                         double2 z, const double (&zz)[NP], bool (&pd)[NP]) {
     if (jb + U < n) {
-      pd = pd_row<KLM, KUM, U>(R, n, jb + U, Ab, AHA, z, zz) && pd;
-      PDUnroll<KLM, KUM, U + 1>::run(R, n, jb, Ab, AHA, z, zz, pd);
+      pd_row<KLM, KUM, NP, U>(R, n, jb + U, Ab, AHA, z, zz, pd);
+      PDUnroll<KLM, KUM, NP, U + 1>::run(R, n, jb, Ab, AHA, z, zz, pd);
     }
   }
 };
-template <int KLM, int KUM>
-struct PDUnroll<KLM, KUM, KLM + KUM> {
-  PSB_HD static void run(PDRing<KLM, KUM>&, int, int, const double2*, const double2*, double2, double, bool&) {}
+template <int KLM, int KUM, int NP>
+struct PDUnroll<KLM, KUM, NP, KLM + KUM> {
+  PSB_HD static void run(PDRing<KLM, KUM> (&)[NP], int, int, const double2*, const double2*, double2,
+                         const double (&)[NP], bool (&)[NP]) {}
 };
 
 template <int KLM, int KUM>
@@ -486,12 +505,12 @@ template <int KLM, int KUM>
 PSB_HD bool pd_test_static(int n, const double2* __restrict__ Ab, const double2* __restrict__ AHA, double2 z,
                            double lam) {
   constexpr int B = KLM + KUM;
-  PDRing<KLM, KUM> R;
-  pd_init(R);
-  const double zz = cnorm2(z) - lam;
-  bool pd = true;
-  for (int jb = 0; jb < n && pd; jb += B) PDUnroll<KLM, KUM, 0>::run(R, n, jb, Ab, AHA, z, zz, pd);
-  return pd;
+  PDRing<KLM, KUM> R[1];
+  pd_init(R[0]);
+  const double zz[1] = {cnorm2(z) - lam};
+  bool pd[1] = {true};
+  for (int jb = 0; jb < n && pd[0]; jb += B) PDUnroll<KLM, KUM, 1, 0>::run(R, n, jb, Ab, AHA, z, zz, pd);
+  return pd[0];
 }
 
 // Runtime-shape PD test (any kl, ku; ring in a caller-provided scratch of b*b complex + 2b doubles).
@@ -543,40 +562,63 @@ PSB_HD bool pd_test_dyn(int n, int kl, int ku, const double2* __restrict__ Ab, c
   return true;
 }
 
-// Bisection state machine of engine B (per point).
-//   phase 0: classify at lam = (tau S)^2: PD -> sigma >= tau S -> search; else hand to engine L
-//   phase 1: geometric search upward (x4 in lambda) until a test fails
-//   phase 2: bisection until (hi - lo) <= rtol * hi; sigma = sqrt((lo + hi) / 2)
-struct BisState {
-  double lo, hi, lam;
-  int phase, tests;
-};
+// Multisection state machine of engine B (per point), NP probes per round.
+//   phase 1: geometric search upward: probes lo*4^(i+1); the first failing probe closes the bracket
+//   phase 2: probes lo + (hi-lo)(i+1)/(NP+1); keep the sub-interval between the last PD probe and
+//            the first non-PD probe; stop when (hi - lo) <= rtol * hi; sigma = sqrt((lo + hi)/2)
+// (The classification test at (tau S)^2 runs first, in its own pass, as phase 0.)
 enum { BIS_CONTINUE = 0, BIS_DONE = 1, BIS_TO_LANCZOS = 2, BIS_FAIL = 3 };
-
-PSB_HD void bis_start(BisState& st, double z_abs, double anorm, double tau) {
-  const double t = tau * (z_abs + anorm);
-  st.lo = 0.0; st.hi = 0.0; st.lam = t * t; st.phase = 0; st.tests = 0;
-}
-PSB_HD int bis_update(BisState& st, bool pd, double rtol, bool force_bisect, int max_tests) {
-  st.tests++;
-  if (st.tests > max_tests) return BIS_FAIL;
-  if (st.phase == 0) {
-    if (!pd) {
-      if (!force_bisect) return BIS_TO_LANCZOS;
-      st.lo = 0.0; st.hi = st.lam; st.phase = 2; st.lam = 0.5 * st.hi; return BIS_CONTINUE;
+struct MsState {
+  double lo, hi;
+  int phase, rounds;
+};
+template <int NP>
+PSB_HD void ms_probes(const MsState& st, double (&lam)[NP]) {
+#pragma unroll
+  for (int i = 0; i < NP; i++) {
+    if (st.phase == 1) {
+      double f = 4.0;
+      for (int t = 0; t < i; t++) f *= 4.0;
+      lam[i] = st.lo * f;
+    } else {
+      lam[i] = st.lo + (st.hi - st.lo) * (double)(i + 1) / (double)(NP + 1);
     }
-    st.lo = st.lam; st.hi = 4.0 * st.lam; st.lam = st.hi; st.phase = 1; return BIS_CONTINUE;
   }
+}
+// returns BIS_CONTINUE / BIS_DONE / BIS_FAIL
+template <int NP>
+PSB_HD int ms_update(MsState& st, const double (&lam)[NP], const bool (&pd)[NP], double rtol, int max_rounds) {
+  st.rounds++;
   if (st.phase == 1) {
-    if (pd) { st.lo = st.hi; st.hi *= 4.0; st.lam = st.hi; return BIS_CONTINUE; }
+    int first_fail = -1;
+#pragma unroll
+    for (int i = NP - 1; i >= 0; i--)
+      if (!pd[i]) first_fail = i;
+    if (first_fail < 0) {
+      st.lo = lam[NP - 1];
+      return st.rounds > max_rounds ? BIS_FAIL : BIS_CONTINUE;
+    }
+    st.hi = lam[first_fail];
+    if (first_fail > 0) st.lo = lam[first_fail - 1];
     st.phase = 2;
   } else {
-    if (pd) st.lo = st.lam; else st.hi = st.lam;
+    double lo = st.lo, hi = st.hi;
+#pragma unroll
+    for (int i = 0; i < NP; i++) {
+      if (pd[i]) lo = fmax(lo, lam[i]);
+      else hi = fmin(hi, lam[i]);
+    }
+    if (lo >= hi) {  // non-monotone answers: the decision is at the rounding level here
+      const double m = 0.5 * (st.lo + st.hi);
+      st.lo = st.hi = m;
+      return BIS_DONE;
+    }
+    st.lo = lo;
+    st.hi = hi;
   }
   if (st.hi - st.lo <= rtol * st.hi) return BIS_DONE;
-  st.lam = 0.5 * (st.lo + st.hi);
-  return BIS_CONTINUE;
+  return st.rounds > max_rounds ? BIS_FAIL : BIS_CONTINUE;
 }
-PSB_HD double bis_sigma(const BisState& st) { return sqrt(0.5 * (st.lo + st.hi)); }
+PSB_HD double ms_sigma(const MsState& st) { return sqrt(0.5 * (st.lo + st.hi)); }
 
 }  // namespace psb

@@ -79,21 +79,17 @@ static int fail(psb_handle* h, int code, const std::string& msg) {
 // runtime-shape (DYN) instantiation.
 typedef void (*bis_fn)(BisArgs);
 typedef void (*lan_fn)(LanArgs);
-struct KPair { int kl, ku; bis_fn b; lan_fn l; int lsmem; };
+// b: classification (NP = 1); bm: multisection (NP probes per thread); l: Lanczos engine.
+struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np; };
 constexpr int kDepth = 8;  // cp.async ring depth of the Lanczos sweeps (rows in flight + 1)
-#define KP(KL, KU) {KL, KU, &k_bisect<KL, KU, false>, &k_lanczos<KL, KU, false, kDepth>, 4 * Ring<KL, KU, kDepth>::BYTES}
-static const KPair kTable[] = {KP(1, 1), KP(1, 3), KP(2, 2), KP(2, 3), KP(3, 3), KP(4, 4), KP(1, 2), KP(2, 1)};
-static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true>, &k_lanczos<16, 16, true, 2>, 0};
-static const KPair kExp[] = {{1, 1, &k_bisect<1, 1, false>, &k_lanczos<1, 1, false, 2>, 4 * Ring<1, 1, 2>::BYTES},
-                             {1, 1, &k_bisect<1, 1, false>, &k_lanczos<1, 1, false, 4>, 4 * Ring<1, 1, 4>::BYTES},
-                             {1, 1, &k_bisect<1, 1, false>, &k_lanczos<1, 1, false, 16>, 4 * Ring<1, 1, 16>::BYTES}};
+#define KP(KL, KU, NP)                                                                            \
+  {KL, KU, &k_bisect<KL, KU, false, 1>, &k_bisect<KL, KU, false, NP>, &k_lanczos<KL, KU, false, kDepth>, \
+   4 * Ring<KL, KU, kDepth>::BYTES, NP}
+static const KPair kTable[] = {KP(1, 1, 2), KP(1, 3, 2), KP(2, 2, 2), KP(2, 3, 1), KP(3, 3, 1), KP(4, 4, 1),
+                               KP(1, 2, 2), KP(2, 1, 2)};
+static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1>, &k_bisect<16, 16, true, 1>,
+                           &k_lanczos<16, 16, true, 2>, 0, 1};
 static KPair pick(int kl, int ku) {
-  if (kl == 1 && ku == 1 && getenv("PSB_DEPTH")) {  // development experiment: ring depth
-    const int d = atoi(getenv("PSB_DEPTH"));
-    if (d == 2) return kExp[0];
-    if (d == 4) return kExp[1];
-    if (d == 16) return kExp[2];
-  }
   for (const KPair& k : kTable)
     if (k.kl == kl && k.ku == ku) return k;
   return kDyn;
@@ -330,9 +326,14 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   if (nB > 0) {
     int occShare = occB;
     if (nA > 0 && occB > 1) occShare = occB - 1;  // leave room for one engine-L block per SM
+    int occM = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, kp.bm, 128, 0));
+    occM = std::max(occM, 1);
+    occShare = (nA > 0 && occM > 1) ? occM - 1 : occM;
     gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, (nB + 127) / 128));
     ba.mode = 1;
-    kp.b<<<(unsigned)gridB, 128, 0, st>>>(ba);
+    ba.max_tests = 200;
+    kp.bm<<<(unsigned)gridB, 128, 0, st>>>(ba);
     CK(cudaGetLastError());
   } else {
     gridB = 0;

@@ -256,7 +256,11 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
 __device__ __forceinline__ int64_t out_index(const int64_t* outidx, int64_t p) { return outidx ? outidx[p] : p; }
 
 // ----------------------------------------------------------------- engine B kernel
-template <int KL, int KU, bool DYN>
+// mode 0 (NP = 1): classification — one LDL^H test per point at lambda = (tau S)^2; PD points go
+//   to listB (sigma >= tau S), the rest to listA (Lanczos engine).
+// mode 1: multisection of the listB points, NP probes per round (NP independent LDL^H chains per
+//   thread share the G row formation and give the FP64 pipe NP-fold instruction-level parallelism).
+template <int KL, int KU, bool DYN, int NP>
 __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   constexpr int B = KL + KU;
   const unsigned FULL = 0xffffffffu;
@@ -264,8 +268,9 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t p = -1;
   double2 z = czero();
-  BisState st;
-  st.lam = 1.0; st.tests = 0; st.phase = 0; st.lo = st.hi = 0.0;
+  MsState st;
+  st.lo = st.hi = 0.0; st.phase = 1; st.rounds = 0;
+  double lam_tau = 0.0;
   bool exhausted = false;
   const int64_t total = (a.mode == 0) ? a.P : (int64_t)a.counters[7];
   while (true) {
@@ -281,14 +286,17 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         if (q < total) {
           const int64_t pt = (a.mode == 0) ? q : a.listB[q];
           z = a.zs[pt];
+          const double t = a.tau * (hypot(z.x, z.y) + a.anorm);
+          lam_tau = t * t;
           if (a.mode == 0 && a.force == 1) {  // Lanczos-only mode: hand over immediately
             unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
             a.listA[slot] = pt;
           } else {
             p = pt;
-            bis_start(st, hypot(z.x, z.y), a.anorm, a.tau);
-            if (a.mode == 1) {  // classification test already passed: lambda_tau is PD
-              st.tests = 1; st.phase = 1; st.lo = st.lam; st.hi = 4.0 * st.lam; st.lam = st.hi;
+            st.rounds = 0;
+            st.lo = lam_tau; st.hi = 4.0 * lam_tau; st.phase = 1;
+            if (a.mode == 1 && a.iters[a.outidx ? a.outidx[pt] : pt] < 0) {  // forced bisection of a point
+              st.lo = 0.0; st.hi = lam_tau; st.phase = 2;                    // that failed classification
             }
           }
         }
@@ -301,26 +309,44 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       continue;
     }
     const bool me = p >= 0;
-    const double lam = me ? st.lam : 1.0;
+    double lam[NP];
+    if (a.mode == 0) {
+#pragma unroll
+      for (int i = 0; i < NP; i++) lam[i] = lam_tau;
+    } else {
+      ms_probes<NP>(st, lam);
+    }
     const double2 zt = me ? z : czero();
-    bool pd = true;
+    bool pd[NP];
+#pragma unroll
+    for (int i = 0; i < NP; i++) { pd[i] = true; if (!me) lam[i] = 1.0; }
     if constexpr (DYN) {
       const int b = a.kl + a.ku;
       LV Ls{a.dyn_L + tid * (int64_t)(b * b > 0 ? b * b : 1), 1};
-      pd = pd_test_dyn(a.n, a.kl, a.ku, a.Ab, a.AHA, zt, lam, Ls, a.dyn_D + tid * (int64_t)(2 * (b > 0 ? b : 1)), 1);
+#pragma unroll
+      for (int i = 0; i < NP; i++)
+        pd[i] = pd_test_dyn(a.n, a.kl, a.ku, a.Ab, a.AHA, zt, lam[i], Ls,
+                            a.dyn_D + tid * (int64_t)(2 * (b > 0 ? b : 1)), 1);
     } else {
-      PDRing<KL, KU> R;
-      pd_init(R);
-      const double zz = cnorm2(zt) - lam;
+      PDRing<KL, KU> R[NP];
+      double zz[NP];
+#pragma unroll
+      for (int i = 0; i < NP; i++) { pd_init(R[i]); zz[i] = cnorm2(zt) - lam[i]; }
       int grp = 0;
       for (int jb = 0; jb < a.n; jb += B) {
-        PDUnroll<KL, KU, 0>::run(R, a.n, jb, a.Ab, a.AHA, zt, zz, pd);
-        if ((++grp & 7) == 0 && !__any_sync(FULL, pd && me)) break;  // every active lane failed
+        PDUnroll<KL, KU, NP, 0>::run(R, a.n, jb, a.Ab, a.AHA, zt, zz, pd);
+        if ((++grp & 7) == 0) {
+          bool any = false;
+#pragma unroll
+          for (int i = 0; i < NP; i++) any = any || pd[i];
+          if (!__any_sync(FULL, any && me)) break;  // every probe of every active lane failed
+        }
       }
     }
     if (me && a.mode == 0) {
       // classification only: PD at (tau S)^2 -> bisection list; else Lanczos list
-      if (pd || a.force == 2) {
+      if (pd[0] || a.force == 2) {
+        if (!pd[0]) a.iters[a.outidx ? a.outidx[p] : p] = -1;  // mark: bracket starts at 0
         unsigned long long slot = atomicAdd(&a.counters[7], 1ull);
         a.listB[slot] = p;
       } else {
@@ -330,19 +356,14 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       p = -1;
     }
     if (me && a.mode == 1) {
-      const int r = bis_update(st, pd, a.rtol, a.force == 2, a.max_tests);
+      const int r = ms_update<NP>(st, lam, pd, a.rtol, a.max_tests);
       if (r == BIS_DONE || r == BIS_FAIL) {
         const int64_t o = out_index(a.outidx, p);
-        a.out[o] = bis_sigma(st);
-        a.iters[o] = st.tests;
+        a.out[o] = ms_sigma(st);
+        a.iters[o] = 1 + st.rounds * NP;  // LDL^H tests incl. the classification test
         a.status[o] = (r == BIS_DONE) ? 1 : 3;
-        atomicAdd(&a.counters[2], (unsigned long long)st.tests);
+        atomicAdd(&a.counters[2], (unsigned long long)(1 + st.rounds * NP));
         atomicAdd(&a.counters[3], 1ull);
-        p = -1;
-      } else if (r == BIS_TO_LANCZOS) {
-        unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
-        a.listA[slot] = p;
-        atomicAdd(&a.counters[2], (unsigned long long)st.tests);
         p = -1;
       }
     }
