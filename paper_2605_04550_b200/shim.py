@@ -1,0 +1,125 @@
+"""Reroute an imported reference package (`pseudospec`) onto the B200 evaluator.
+
+The reference has no plugin registry or FFI: its σ callers look `smin_many`,
+`full_pseudospectrum` and `restricted_field` up as module globals (core.py:187,207;
+pipeline.py:17-18; cli.py:22), and the predictor through `pipeline._predict_points`
+(pipeline.py:179,200,222). `install()` rebinds exactly those names (the substitution-point
+precedent is the reference's own tests, tests/test_pipeline.py:188 monkeypatching
+`pipeline.predict_map`), so every caller — cmd_compute, build_dataset, calibrate_threshold,
+hybrid_pseudospectrum, benchmark — runs on the GPU unchanged. Results come back as the
+reference's own types (SigmaField) and failures as its own exceptions (ParameterError,
+NumericalError). `uninstall()` restores the originals.
+
+    import pseudospec
+    from paper_2605_04550_b200 import shim
+    shim.install(pseudospec)
+    pseudospec.pipeline.benchmark(bundle, corpus, grid, eps)   # σ sweeps and NN on the B200
+"""
+
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+
+from . import core, pipeline
+
+_saved: list[tuple[object, str, object]] = []
+
+
+def _translate(ref_core):
+    """Map this package's exceptions onto the reference's classes."""
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrapped(*a, **k):
+            try:
+                return fn(*a, **k)
+            except core.ParameterError as e:
+                raise ref_core.ParameterError(str(e)) from e
+            except core.NumericalError as e:
+                raise ref_core.NumericalError(str(e)) from e
+        return wrapped
+    return deco
+
+
+def _patch(module, name, value):
+    _saved.append((module, name, getattr(module, name)))
+    setattr(module, name, value)
+
+
+def install(ps=None, predictor: bool = True):
+    """Rebind the reference's σ entry points (and, by default, its predictor) to this package."""
+    if ps is None:
+        import pseudospec as ps  # noqa: F811
+    import importlib
+    rcore = importlib.import_module(ps.__name__ + ".core")
+    rpipe = importlib.import_module(ps.__name__ + ".pipeline")
+    rcli = importlib.import_module(ps.__name__ + ".cli")
+    tr = _translate(rcore)
+
+    def _real(A):
+        # the reference validates with require_real_matrix (core.py:112-119); keep that contract
+        return A if isinstance(A, core.BandMatrix) else rcore.require_real_matrix(A)
+
+    @tr
+    def smin_many(A, zs, label="matrix", chunk=512):
+        return core.smin_many(_real(A), zs, label=label)
+
+    @tr
+    def smin_at(A, z, label="matrix"):
+        return core.smin_at(_real(A), z, label=label)
+
+    @tr
+    def full_pseudospectrum(A, grid, label="matrix", workers=1):
+        vals = core.full_pseudospectrum(_real(A), core.make_grid(grid.x_min, grid.x_max, grid.y_min, grid.y_max,
+                                                                 grid.nx, grid.ny), label=label).values
+        return rcore.SigmaField(grid, vals)
+
+    @tr
+    def restricted_field(A, grid, region, label="matrix"):
+        region = rcore._check_mask(region, grid.shape)
+        g = core.make_grid(grid.x_min, grid.x_max, grid.y_min, grid.y_max, grid.nx, grid.ny)
+        return rcore.SigmaField(grid, core.restricted_field(_real(A), g, region, label=label).values)
+
+    for mod in (rcore,):
+        _patch(mod, "smin_many", smin_many)
+        _patch(mod, "smin_at", smin_at)
+    for mod in (rcore, rpipe, rcli):
+        _patch(mod, "full_pseudospectrum", full_pseudospectrum)
+    for mod in (rcore, rpipe):
+        _patch(mod, "restricted_field", restricted_field)
+    if hasattr(ps, "smin_many"):
+        for name, fn in (("smin_many", smin_many), ("smin_at", smin_at),
+                         ("full_pseudospectrum", full_pseudospectrum), ("restricted_field", restricted_field)):
+            _patch(ps, name, fn)
+
+    if predictor:
+        cache: dict[int, pipeline.ModelBundle] = {}
+
+        @tr
+        def _predict_points(bundle, gf, zs):
+            ours = cache.get(id(bundle))
+            if ours is None or ours.tau_star != bundle.tau_star:
+                ours = pipeline.ModelBundle.from_reference(bundle)
+                cache[id(bundle)] = ours
+            return pipeline._predict_points(ours, gf, np.asarray(zs, dtype=complex))
+
+        @tr
+        def predicted_region(prob_field, tau):
+            if not 0 < tau < 1:
+                raise rcore.ParameterError(f"tau must lie in (0, 1), got {tau}")
+            return pipeline.predicted_region(prob_field, tau)
+
+        _patch(rpipe, "_predict_points", _predict_points)
+        _patch(rpipe, "predicted_region", predicted_region)
+    return ps
+
+
+def uninstall():
+    while _saved:
+        module, name, value = _saved.pop()
+        setattr(module, name, value)
+
+
+def installed() -> bool:
+    return bool(_saved)

@@ -40,3 +40,16 @@ def gpu():
     """Library handle on cuda:0; on a GPU box a missing library is a failure, not a skip."""
     from paper_2605_04550_b200 import _lib
     return _lib.handle(0)
+
+
+@pytest.fixture(scope="session")
+def refpkg_any():
+    """The unmodified reference package from baseline/_ref (travels to the GPU box) or the
+    read-only checkout; skip when neither exists."""
+    for cand in (ROOT / "baseline" / "_ref", REF_SRC):
+        if (cand / "pseudospec").exists():
+            if str(cand) not in sys.path:
+                sys.path.insert(0, str(cand))
+            import pseudospec
+            return pseudospec
+    pytest.skip("reference package not available")
