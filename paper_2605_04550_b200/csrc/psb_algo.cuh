@@ -71,6 +71,32 @@ PSB_HD double2 crcp(double2 d) {
   }
 }
 
+// 1/d = conj(d) / |d|^2 with a MUFU-seeded reciprocal (about 1 ulp) when |d|^2 is safely inside
+// the normal range; Smith's scaled division otherwise.
+// Reciprocal for the LDL^H pivots: MUFU seed + two Newton steps (~1 ulp; the PD decision only
+// needs the sign of every pivot, and L = s / D is insensitive to an ulp in 1/D).
+PSB_HD double fast_rcp(double x) {
+#ifdef __CUDA_ARCH__
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+
+PSB_HD double2 crcp_fast(double2 d) {
+  const double m = fmax(fabs(d.x), fabs(d.y));
+  if (m > 1e-150 && m < 1e150) {
+    const double r = fast_rcp(fma(d.x, d.x, d.y * d.y));
+    return cmk(d.x * r, -d.y * r);
+  }
+  return crcp(d);
+}
+
 // Lane view of a lane-interleaved array: element i lives at p[i * ld].
 struct LV {
   double2* p;
@@ -152,7 +178,7 @@ PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z,
     double2 d = win[0][0];
     double2 ri;
     if (d.x == 0.0 && d.y == 0.0) { ok = false; ri = czero(); }
-    else ri = crcp(d);
+    else ri = crcp_fast(d);
     const int64_t rb = (int64_t)j * NU;
 #pragma unroll
     for (int c = 1; c <= WM; c++)
@@ -424,21 +450,6 @@ PSB_HD double2 g_entry(int n, int j, int d, const double2* __restrict__ Ab, cons
   return v;
 }
 
-// Reciprocal for the LDL^H pivots: MUFU seed + two Newton steps (~1 ulp; the PD decision only
-// needs the sign of every pivot, and L = s / D is insensitive to an ulp in 1/D).
-PSB_HD double fast_rcp(double x) {
-#ifdef __CUDA_ARCH__
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-#else
-  return 1.0 / x;
-#endif
-}
-
 // One row of the factorization for static shapes, for NP independent shifts lambda_q that share
 // the off-diagonal G entries (only the diagonal depends on lambda). U = j mod B (compile-time).
 template <int KLM, int KUM, int NP, int U>
@@ -486,6 +497,82 @@ struct PDUnroll<KLM, KUM, NP, KLM + KUM> {
   PSB_HD static void run(PDRing<KLM, KUM> (&)[NP], int, int, const double2*, const double2*, double2,
                          const double (&)[NP], bool (&)[NP]) {}
 };
+
+// Right-looking (outer-product) banded LDL^H with a sliding lower (b+1)x(b+1) window of the
+// partially eliminated Schur complement: W[r][c] = entry (j+r, j+c), c <= r. Step j takes the pivot
+// D_j = W[0][0], scales column 0 and updates the trailing window; the next pivot is
+// D_{j+1} = W[1][1] - |W[1][0]|^2 / D_j, so the dependency chain per row is one reciprocal plus one
+// FMA (the left-looking form chains through all b multipliers of the row). Same arithmetic test.
+template <int KLM, int KUM>
+struct PDWin {
+  static constexpr int B = KLM + KUM;
+  double2 W[B + 1][B + 1];
+};
+
+template <int KLM, int KUM, int NP>
+PSB_HD void pdw_load_row(PDWin<KLM, KUM> (&Wn)[NP], int r, int n, int i, const double2* __restrict__ Ab,
+                         const double2* __restrict__ AHA, double2 z, const double (&zz)[NP]) {
+  // row r of the window = matrix row i, columns i-r .. i (G entries G[i, i-d], d = r - c)
+  constexpr int B = KLM + KUM;
+  double2 g[B + 1];
+#pragma unroll
+  for (int d = 0; d <= B; d++) {
+    g[d] = czero();
+    if (d <= r && i < n && i - d >= 0) g[d] = g_entry<KLM, KUM>(n, i, d, Ab, AHA, z, 0.0);
+  }
+#pragma unroll
+  for (int q = 0; q < NP; q++) {
+#pragma unroll
+    for (int c = 0; c <= B; c++)
+      if (c <= r) Wn[q].W[r][c] = g[r - c];
+    Wn[q].W[r][r].x += (i < n) ? zz[q] : 1.0;  // rows past n: identity padding (PD-neutral)
+    Wn[q].W[r][r].y = 0.0;
+  }
+}
+
+template <int KLM, int KUM, int NP>
+PSB_HD void pdw_step(PDWin<KLM, KUM> (&Wn)[NP], bool (&pd)[NP]) {
+  constexpr int B = KLM + KUM;
+#pragma unroll
+  for (int q = 0; q < NP; q++) {
+    auto& W = Wn[q].W;
+    const double dj = W[0][0].x;
+    pd[q] = pd[q] && (dj > 0.0);
+    const double iD = fast_rcp(dj);
+    double2 l[B + 1];
+#pragma unroll
+    for (int r = 1; r <= B; r++) l[r] = cscale(W[r][0], iD);
+    // next pivot first (critical path), then the rest of the trailing update
+    W[1][1].x = fma(-l[1].x, W[1][0].x, fma(-l[1].y, W[1][0].y, W[1][1].x));
+#pragma unroll
+    for (int r = 2; r <= B; r++) {
+#pragma unroll
+      for (int c = 1; c < r; c++) W[r][c] = cfms(W[r][c], l[r], cconj(W[c][0]));
+      W[r][r].x = fma(-l[r].x, W[r][0].x, fma(-l[r].y, W[r][0].y, W[r][r].x));
+    }
+#pragma unroll
+    for (int r = 1; r <= B; r++)
+#pragma unroll
+      for (int c = 1; c <= r; c++) W[r - 1][c - 1] = W[r][c];
+  }
+}
+
+// Whole PD test (right-looking) for NP shifts; `vote` lets device callers exit early.
+template <int KLM, int KUM, int NP>
+PSB_HD void pdw_test(int n, const double2* __restrict__ Ab, const double2* __restrict__ AHA, double2 z,
+                     const double (&lam)[NP], bool (&pd)[NP]) {
+  constexpr int B = KLM + KUM;
+  PDWin<KLM, KUM> Wn[NP];
+  double zz[NP];
+#pragma unroll
+  for (int q = 0; q < NP; q++) { zz[q] = cnorm2(z) - lam[q]; pd[q] = true; }
+#pragma unroll
+  for (int r = 0; r <= B; r++) pdw_load_row<KLM, KUM, NP>(Wn, r, n, r, Ab, AHA, z, zz);
+  for (int j = 0; j < n; j++) {
+    pdw_step<KLM, KUM, NP>(Wn, pd);
+    pdw_load_row<KLM, KUM, NP>(Wn, B, n, j + 1 + B, Ab, AHA, z, zz);
+  }
+}
 
 template <int KLM, int KUM>
 PSB_HD void pd_init(PDRing<KLM, KUM>& R) {

@@ -80,16 +80,23 @@ static int fail(psb_handle* h, int code, const std::string& msg) {
 typedef void (*bis_fn)(BisArgs);
 typedef void (*lan_fn)(LanArgs);
 // b: classification (NP = 1); bm: multisection (NP probes per thread); l: Lanczos engine.
-struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np; };
+struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np, g; };
 constexpr int kDepth = 8;  // cp.async ring depth of the Lanczos sweeps (rows in flight + 1)
-#define KP(KL, KU, NP)                                                                            \
-  {KL, KU, &k_bisect<KL, KU, false, 1>, &k_bisect<KL, KU, false, NP>, &k_lanczos<KL, KU, false, kDepth>, \
-   4 * Ring<KL, KU, kDepth>::BYTES, NP}
-static const KPair kTable[] = {KP(1, 1, 2), KP(1, 3, 2), KP(2, 2, 2), KP(2, 3, 1), KP(3, 3, 1), KP(4, 4, 1),
-                               KP(1, 2, 2), KP(2, 1, 2)};
-static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1>, &k_bisect<16, 16, true, 1>,
-                           &k_lanczos<16, 16, true, 2>, 0, 1};
+// (NP probes per lane) x (G lanes per point), fixed per band shape (results must not depend on the batch)
+#define KP(KL, KU, NP, G)                                                                               \
+  {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, kDepth>, \
+   4 * Ring<KL, KU, kDepth>::BYTES, NP, G}
+static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 2, 2, 1), KP(2, 3, 1, 1), KP(3, 3, 1, 1),
+                               KP(4, 4, 1, 1), KP(1, 2, 2, 1), KP(2, 1, 2, 1)};
+static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,
+                           &k_lanczos<16, 16, true, 2>, 0, 1, 1};
+static const KPair kAlt[] = {KP(1, 3, 1, 1), KP(1, 3, 1, 2), KP(1, 3, 3, 1), KP(2, 3, 2, 1), KP(3, 3, 2, 1)};
 static KPair pick(int kl, int ku) {
+  if (getenv("PSB_ALT")) {  // development A/B of the (NP, G) choice
+    const int v = atoi(getenv("PSB_ALT"));
+    for (const KPair& k : kAlt)
+      if (k.kl == kl && k.ku == ku && (v == k.np * 10 + k.g)) return k;
+  }
   for (const KPair& k : kTable)
     if (k.kl == kl && k.ku == ku) return k;
   return kDyn;
@@ -194,10 +201,16 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
   CK(cudaSetDevice(h->device));
   CK(h->Ab.ensure(sizeof(cd) * nd * n));
   CK(h->AHA.ensure(sizeof(cd) * (b + 1) * n));
-  CK(h->v1.ensure(sizeof(cd) * n));
+  CK(h->v1.ensure(sizeof(cd) * n * 33));
   CK(cudaMemcpyAsync(h->Ab.p, band, sizeof(cd) * nd * n, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(h->AHA.p, aha.data(), sizeof(cd) * (b + 1) * n, cudaMemcpyHostToDevice, h->stream));
-  CK(cudaMemcpyAsync(h->v1.p, v1.data(), sizeof(cd) * n, cudaMemcpyHostToDevice, h->stream));
+  // [0, n): v1; [n, 33n): v1 replicated per lane (v1rep[j*32 + lane]) for coalesced cp.async
+  std::vector<cd> v1x((size_t)n * 33);
+  for (int i = 0; i < n; i++) {
+    v1x[i] = v1[i];
+    for (int l = 0; l < 32; l++) v1x[(size_t)n + (size_t)i * 32 + l] = v1[i];
+  }
+  CK(cudaMemcpyAsync(h->v1.p, v1x.data(), sizeof(cd) * n * 33, cudaMemcpyHostToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   h->n = n; h->kl = kl; h->ku = ku;
   h->anorm = std::sqrt(n1 * ni);
@@ -304,7 +317,8 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     CK(h->scratch.ensure((size_t)(warps * warp_stride * sizeof(double2))));
     CK(h->pivs.ensure((size_t)(warps * piv_stride * 4)));
     LanArgs la;
-    la.s = s; la.Ab = h->Ab.as<double2>(); la.v1 = h->v1.as<double2>();
+    la.s = s; la.Ab = h->Ab.as<double2>();
+    la.v1 = dyn ? h->v1.as<double2>() : h->v1.as<double2>() + n;  // pipelined sweeps read the replicated copy
     la.zs = d_zs; la.outidx = d_outidx; la.listA = h->listA.as<int64_t>(); la.counters = cnt;
     la.out = d_out; la.iters = d_iters; la.status = d_status;
     la.scratch = h->scratch.as<double2>(); la.pivs = h->pivs.as<int>();
@@ -330,7 +344,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, kp.bm, 128, 0));
     occM = std::max(occM, 1);
     occShare = (nA > 0 && occM > 1) ? occM - 1 : occM;
-    gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, (nB + 127) / 128));
+    gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, (nB * kp.g + 127) / 128));
     ba.mode = 1;
     ba.max_tests = 200;
     kp.bm<<<(unsigned)gridB, 128, 0, st>>>(ba);

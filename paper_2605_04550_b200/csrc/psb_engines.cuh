@@ -91,6 +91,8 @@ __device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV 
         cp16(R.at(sl, NU), T.p + (int64_t)j * 32);
         cp16(R.at(sl, NU + 1), RA.p + (int64_t)j * 32);
         if (k >= 3) cp16(R.at(sl, NU + 2), RB.p + (int64_t)j * 32);
+      } else {
+        cp16(R.at(sl, NU), v1 + (int64_t)j * 32 + R.lane);  // start vector, lane-replicated copy
       }
     }
     cp_commit();
@@ -107,7 +109,7 @@ __device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV 
     const int sl = j % D;
     double2 r;
     if (k == 1) {
-      r = v1[j];
+      r = *R.at(sl, NU);
       RA.put(j, r);
     } else {
       const double2 ra = *R.at(sl, NU + 1);
@@ -256,48 +258,57 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
 __device__ __forceinline__ int64_t out_index(const int64_t* outidx, int64_t p) { return outidx ? outidx[p] : p; }
 
 // ----------------------------------------------------------------- engine B kernel
-// mode 0 (NP = 1): classification — one LDL^H test per point at lambda = (tau S)^2; PD points go
-//   to listB (sigma >= tau S), the rest to listA (Lanczos engine).
-// mode 1: multisection of the listB points, NP probes per round (NP independent LDL^H chains per
-//   thread share the G row formation and give the FP64 pipe NP-fold instruction-level parallelism).
-template <int KL, int KU, bool DYN, int NP>
+// mode 0 (NP = G = 1): classification — one LDL^H test per point at lambda = (tau S)^2; PD points
+//   go to listB (sigma >= tau S), the rest to listA (Lanczos engine).
+// mode 1: multisection of the listB points. A group of G lanes owns one point and every lane runs NP
+//   independent LDL^H chains (sharing the G-row formation), so a round tests K = G*NP shifts:
+//   search rounds probe lo*4^(i+1), then the bracket [lo, hi] is cut at lo + (hi-lo)(i+1)/(K+1).
+//   The group keeps [max PD probe, min non-PD probe] (shuffle reductions), so the bracket shrinks
+//   (K+1)-fold per round. (G, NP) depend only on the band shape, never on the batch, so every sigma
+//   is a pure function of (A, z).
+template <int KL, int KU, bool DYN, int NP, int G>
 __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   constexpr int B = KL + KU;
+  constexpr int K = NP * G;
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  const int gl = lane % G;               // lane within the group
+  const int leader = lane - gl;          // group leader lane
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t p = -1;
   double2 z = czero();
-  MsState st;
-  st.lo = st.hi = 0.0; st.phase = 1; st.rounds = 0;
-  double lam_tau = 0.0;
+  double lo = 0.0, hi = 0.0;
+  int phase = 1, rounds = 0;
   bool exhausted = false;
   const int64_t total = (a.mode == 0) ? a.P : (int64_t)a.counters[7];
   while (true) {
-    unsigned idle = __ballot_sync(FULL, p < 0);
+    const unsigned idle = __ballot_sync(FULL, p < 0 && gl == 0);  // idle groups (leader bits)
     if (idle && !exhausted) {
       const int cnt = __popc(idle);
       unsigned long long base = 0;
       if (lane == 0) base = atomicAdd(&a.counters[0], (unsigned long long)cnt);
       base = __shfl_sync(FULL, base, 0);
-      if (p < 0) {
-        const int rank = __popc(idle & ((1u << lane) - 1u));
+      const int rank = __popc(idle & ((1u << leader) - 1u));
+      const bool grp_idle = (idle >> leader) & 1u;
+      if (grp_idle) {
         const int64_t q = (int64_t)base + rank;
         if (q < total) {
-          const int64_t pt = (a.mode == 0) ? q : a.listB[q];
+          const int64_t entry = (a.mode == 0) ? q : a.listB[q];
+          const bool forced = entry < 0;          // forced bisection of a point that failed classification
+          const int64_t pt = forced ? ~entry : entry;
           z = a.zs[pt];
           const double t = a.tau * (hypot(z.x, z.y) + a.anorm);
-          lam_tau = t * t;
+          const double lam_tau = t * t;
           if (a.mode == 0 && a.force == 1) {  // Lanczos-only mode: hand over immediately
-            unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
-            a.listA[slot] = pt;
+            if (gl == 0) {
+              unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
+              a.listA[slot] = pt;
+            }
           } else {
             p = pt;
-            st.rounds = 0;
-            st.lo = lam_tau; st.hi = 4.0 * lam_tau; st.phase = 1;
-            if (a.mode == 1 && a.iters[a.outidx ? a.outidx[pt] : pt] < 0) {  // forced bisection of a point
-              st.lo = 0.0; st.hi = lam_tau; st.phase = 2;                    // that failed classification
-            }
+            rounds = 0;
+            lo = lam_tau; hi = INFINITY; phase = 1;
+            if (a.mode == 1 && forced) { lo = 0.0; hi = lam_tau; phase = 2; }
           }
         }
       }
@@ -310,60 +321,96 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
     }
     const bool me = p >= 0;
     double lam[NP];
-    if (a.mode == 0) {
 #pragma unroll
-      for (int i = 0; i < NP; i++) lam[i] = lam_tau;
-    } else {
-      ms_probes<NP>(st, lam);
+    for (int q = 0; q < NP; q++) {
+      const int i = gl * NP + q;
+      if (a.mode == 0) lam[q] = lo;
+      else if (phase == 1) lam[q] = lo * exp2(2.0 * (i + 1));
+      else lam[q] = lo + (hi - lo) * (double)(i + 1) / (double)(K + 1);
+      if (!me) lam[q] = 1.0;
     }
     const double2 zt = me ? z : czero();
     bool pd[NP];
 #pragma unroll
-    for (int i = 0; i < NP; i++) { pd[i] = true; if (!me) lam[i] = 1.0; }
+    for (int q = 0; q < NP; q++) pd[q] = true;
     if constexpr (DYN) {
       const int b = a.kl + a.ku;
       LV Ls{a.dyn_L + tid * (int64_t)(b * b > 0 ? b * b : 1), 1};
 #pragma unroll
-      for (int i = 0; i < NP; i++)
-        pd[i] = pd_test_dyn(a.n, a.kl, a.ku, a.Ab, a.AHA, zt, lam[i], Ls,
+      for (int q = 0; q < NP; q++)
+        pd[q] = pd_test_dyn(a.n, a.kl, a.ku, a.Ab, a.AHA, zt, lam[q], Ls,
                             a.dyn_D + tid * (int64_t)(2 * (b > 0 ? b : 1)), 1);
     } else {
-      PDRing<KL, KU> R[NP];
+      PDWin<KL, KU> Wn[NP];
       double zz[NP];
 #pragma unroll
-      for (int i = 0; i < NP; i++) { pd_init(R[i]); zz[i] = cnorm2(zt) - lam[i]; }
-      int grp = 0;
-      for (int jb = 0; jb < a.n; jb += B) {
-        PDUnroll<KL, KU, NP, 0>::run(R, a.n, jb, a.Ab, a.AHA, zt, zz, pd);
-        if ((++grp & 7) == 0) {
+      for (int q = 0; q < NP; q++) zz[q] = cnorm2(zt) - lam[q];
+#pragma unroll
+      for (int r = 0; r <= B; r++) pdw_load_row<KL, KU, NP>(Wn, r, a.n, r, a.Ab, a.AHA, zt, zz);
+#pragma unroll 4
+      for (int j = 0; j < a.n; j++) {
+        pdw_step<KL, KU, NP>(Wn, pd);
+        pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + 1 + B, a.Ab, a.AHA, zt, zz);
+        if ((j & 31) == 31) {
           bool any = false;
 #pragma unroll
-          for (int i = 0; i < NP; i++) any = any || pd[i];
+          for (int q = 0; q < NP; q++) any = any || pd[q];
           if (!__any_sync(FULL, any && me)) break;  // every probe of every active lane failed
         }
       }
     }
-    if (me && a.mode == 0) {
-      // classification only: PD at (tau S)^2 -> bisection list; else Lanczos list
-      if (pd[0] || a.force == 2) {
-        if (!pd[0]) a.iters[a.outidx ? a.outidx[p] : p] = -1;  // mark: bracket starts at 0
-        unsigned long long slot = atomicAdd(&a.counters[7], 1ull);
-        a.listB[slot] = p;
-      } else {
-        unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
-        a.listA[slot] = p;
+    if (a.mode == 0) {
+      if (me) {
+        if (pd[0] || a.force == 2) {
+          unsigned long long slot = atomicAdd(&a.counters[7], 1ull);
+          a.listB[slot] = pd[0] ? p : ~p;  // ~p: bracket starts at 0 (forced bisection)
+        } else {
+          unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
+          a.listA[slot] = p;
+        }
+        p = -1;
       }
-      p = -1;
+      continue;
     }
-    if (me && a.mode == 1) {
-      const int r = ms_update<NP>(st, lam, pd, a.rtol, a.max_tests);
-      if (r == BIS_DONE || r == BIS_FAIL) {
-        const int64_t o = out_index(a.outidx, p);
-        a.out[o] = ms_sigma(st);
-        a.iters[o] = 1 + st.rounds * NP;  // LDL^H tests incl. the classification test
-        a.status[o] = (r == BIS_DONE) ? 1 : 3;
-        atomicAdd(&a.counters[2], (unsigned long long)(1 + st.rounds * NP));
-        atomicAdd(&a.counters[3], 1ull);
+    // ---- mode 1: combine the group's K answers into the new bracket
+    double plo = -INFINITY, phi = INFINITY;
+#pragma unroll
+    for (int q = 0; q < NP; q++) {
+      if (pd[q]) plo = fmax(plo, lam[q]);
+      else phi = fmin(phi, lam[q]);
+    }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) {
+      plo = fmax(plo, __shfl_xor_sync(FULL, plo, off, G));
+      phi = fmin(phi, __shfl_xor_sync(FULL, phi, off, G));
+    }
+    if (me) {
+      rounds++;
+      int r = BIS_CONTINUE;
+      const double nlo = fmax(lo, plo), nhi = fmin(hi, phi);
+      if (phase == 1 && phi == INFINITY) {
+        lo = nlo;  // every probe PD: keep searching upward
+      } else {
+        phase = 2;
+        if (nlo >= nhi) {  // non-monotone answers: the decision is at the rounding level here
+          lo = hi = 0.5 * (lo + (hi == INFINITY ? phi : hi));
+          r = BIS_DONE;
+        } else {
+          lo = nlo;
+          hi = nhi;
+          if (hi - lo <= a.rtol * hi) r = BIS_DONE;
+        }
+      }
+      if (r == BIS_CONTINUE && rounds >= a.max_tests) r = BIS_FAIL;
+      if (r != BIS_CONTINUE) {
+        if (gl == 0) {
+          const int64_t o = out_index(a.outidx, p);
+          a.out[o] = sqrt(0.5 * (lo + hi));
+          a.iters[o] = 1 + rounds * K;  // LDL^H tests incl. the classification test
+          a.status[o] = (r == BIS_DONE) ? 1 : 3;
+          atomicAdd(&a.counters[2], (unsigned long long)(1 + rounds * K));
+          atomicAdd(&a.counters[3], 1ull);
+        }
         p = -1;
       }
     }

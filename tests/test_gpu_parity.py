@@ -168,3 +168,15 @@ def test_edge_cases(gpu):
     diag = np.diag(np.arange(1.0, 6.0))  # kl = ku = 0
     assert np.allclose(core.smin_many(diag, [2.5 + 0j, 10j]),
                        [0.5, np.abs(10j - np.arange(1, 6)).min()], rtol=1e-12)
+
+
+def test_no_state_leaks_between_calls(gpu):
+    """Scratch buffers are reused across calls: a forced-engine call, another matrix, or a smaller batch
+    must not change the next call's bits (regression: a stale per-point marker once did)."""
+    A = configs.CONFIGS["C1"].matrix()
+    zs = configs.CONFIGS["C1"].grid.points().ravel()
+    base = core.smin_many(A, zs)
+    core.smin_many(A, zs, opts=_lib.make_opts(force_engine=2))
+    core.smin_many(configs.CONFIGS["C4"].matrix(), configs.CONFIGS["C4"].grid.points().ravel()[:64])
+    core.smin_many(A, zs[:7], opts=_lib.make_opts(force_engine=1))
+    assert np.array_equal(core.smin_many(A, zs), base)
