@@ -360,16 +360,22 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       }
     }
     if (a.mode == 0) {
-      if (me) {
-        if (pd[0] || a.force == 2) {
-          unsigned long long slot = atomicAdd(&a.counters[7], 1ull);
-          a.listB[slot] = pd[0] ? p : ~p;  // ~p: bracket starts at 0 (forced bisection)
-        } else {
-          unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
-          a.listA[slot] = p;
-        }
-        p = -1;
+      // warp-aggregated appends keep a warp's consecutive (spatially adjacent) points together in
+      // the lists, so engine-L warps get points with similar step counts (less lane divergence)
+      const bool toB = me && (pd[0] || a.force == 2);
+      const bool toA = me && !toB;
+      const unsigned mA = __ballot_sync(FULL, toA), mB = __ballot_sync(FULL, toB);
+      unsigned long long bA = 0, bB = 0;
+      if (lane == 0) {
+        if (mA) bA = atomicAdd(&a.counters[1], (unsigned long long)__popc(mA));
+        if (mB) bB = atomicAdd(&a.counters[7], (unsigned long long)__popc(mB));
       }
+      bA = __shfl_sync(FULL, bA, 0);
+      bB = __shfl_sync(FULL, bB, 0);
+      const unsigned below = (1u << lane) - 1u;
+      if (toA) a.listA[bA + __popc(mA & below)] = p;
+      if (toB) a.listB[bB + __popc(mB & below)] = pd[0] ? p : ~p;  // ~p: bracket starts at 0 (forced)
+      if (me) p = -1;
       continue;
     }
     // ---- mode 1: combine the group's K answers into the new bracket
