@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", help="workload (C1..C4); C2 is the headline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-guided", action="store_true")
     return ap.parse_args()
 
 
@@ -69,7 +70,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
             return
@@ -160,6 +161,45 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------- our arm
+def run_guided(cfg, grid, args) -> dict:
+    """BASELINE C2's MLP-guided run (pipeline.py:273-297): hierarchical prediction (K2) with the bundle
+    the reference trained and calibrated (tests/golden/model_grcar.npz), 5x5-dilated region, restricted
+    σ sweep (K1). Reports the reference's own timing split (t_nn incl. the host O(n^3) global_features,
+    t_restricted) and its metrics against the full map (pipeline.py:300-331)."""
+    import torch
+
+    from paper_2605_04550_b200 import core, pipeline
+    bundle = pipeline.load_npz(ROOT / "tests" / "golden" / "model_grcar.npz")
+    A = cfg.matrix(0).todense().real
+    eps = 0.01
+    res = None
+    t_nn, t_r = [], []
+    for it in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        res = pipeline.hybrid_pseudospectrum(bundle, A, grid, eps=eps)
+        if it >= args.warmup:
+            t_nn.append(res.t_nn)
+            t_r.append(res.t_restricted)
+    gf_t = time.perf_counter()
+    pipeline.global_features(A)
+    gf_t = time.perf_counter() - gf_t
+    full = core.full_pseudospectrum(cfg.matrix(0), grid)
+    truth = full.values <= eps
+    region = res.region
+    tp = int((region & truth).sum())
+    dil = core.dilate(truth, 3)
+    recall = float((region & dil).sum() / dil.sum()) if dil.sum() else 1.0
+    coverage = float(tp / truth.sum()) if truth.sum() else 1.0
+    same = bool(np.array_equal(res.field.values[region], full.values[region]))
+    tn, tr = float(np.median(t_nn)), float(np.median(t_r))
+    return {"eps": eps, "tau_star": bundle.tau_star, "nn_evaluations": int(res.nn_evaluations),
+            "grid_fraction": float(region.mean()), "t_nn_s": tn, "t_global_features_host_s": gf_t,
+            "t_restricted_s": tr, "t_hybrid_s": tn + tr,
+            "grid_points_per_s": grid.size / (tn + tr), "recall": recall, "coverage": coverage,
+            "restricted_equals_full_bitwise": same,
+            "note": "t_nn includes the host O(n^3) global_features (eig/svd, SURVEY 8f row 1)"}
+
+
 def run_ours(args, rank, world, local_rank):
     import ctypes as C
 
@@ -201,6 +241,9 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    sampler = ClockSampler(local_rank)  # covers warm-up, the timed steps and the e2e leg
+    sampler.start()
+    time.sleep(0.3)
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
@@ -208,8 +251,6 @@ def run_ours(args, rank, world, local_rank):
     st = d_status.cpu().numpy()
     assert (st <= 2).all(), "non-converged points in the benchmark step"
 
-    sampler = ClockSampler(local_rank)
-    sampler.start()
     stats = []
     step_ms = []
     barrier()
@@ -226,7 +267,6 @@ def run_ours(args, rank, world, local_rank):
         stats.append(h.stats())
     torch.cuda.synchronize()
     barrier()
-    clocks = sampler.stop()
 
     ms_local = float(np.mean(step_ms))
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
@@ -249,6 +289,7 @@ def run_ours(args, rank, world, local_rank):
         dt = (time.perf_counter() - t0) * 1e3
         if it >= args.warmup:
             e2e_ms.append(dt)
+    clocks = sampler.stop()
     te = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -289,6 +330,10 @@ def run_ours(args, rank, world, local_rank):
     flops_pt = (s["flops_bisect"] + s["flops_lanczos"]) / max(1, s["n_points"])
     roof_pts = fp64_peak * 1e12 / flops_pt if flops_pt > 0 else None
 
+    guided = None
+    if rank == 0 and world == 1 and args.config in ("C1", "C2") and not args.no_guided:
+        guided = run_guided(cfg, grid, args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         Ad = A.todense()
@@ -325,6 +370,8 @@ def run_ours(args, rank, world, local_rank):
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if guided:
+            line["guided"] = guided
         print(json.dumps(line), flush=True)
 
 

@@ -103,6 +103,7 @@ __device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV 
   double bsq = 0.0;
 #pragma unroll
   for (int q = 0; q < D - 1; q++) issue(q);
+#pragma unroll 2
   for (int j = 0; j < n; j++) {
     issue(j + D - 1);
     cp_wait<D - 1>();
@@ -151,6 +152,7 @@ __device__ double pl_s2(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T) {
   double nrm = 0.0;
 #pragma unroll
   for (int q = 0; q < D - 1; q++) issue(q);
+#pragma unroll 2
   for (int q = 0; q < n; q++) {
     const int j = n - 1 - q;
     issue(q + D - 1);
@@ -196,6 +198,7 @@ __device__ void pl_s3(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T, dou
   for (int r = 0; r <= KL; r++) bw[r] = (r < n) ? cscale(T.get(r), scale) : czero();
 #pragma unroll
   for (int q = 0; q < D - 1; q++) issue(q);
+#pragma unroll 2
   for (int j = 0; j < n; j++) {
     issue(j + D - 1);
     cp_wait<D - 1>();
@@ -237,6 +240,7 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
   double acc = 0.0;
 #pragma unroll
   for (int q = 0; q < D - 1; q++) issue(q);
+#pragma unroll 2
   for (int q = 0; q < n; q++) {
     const int j = n - 1 - q;
     issue(q + D - 1);
