@@ -530,14 +530,39 @@ PSB_HD void pdw_load_row(PDWin<KLM, KUM> (&Wn)[NP], int r, int n, int i, const d
   }
 }
 
-template <int KLM, int KUM, int NP>
-PSB_HD void pdw_step(PDWin<KLM, KUM> (&Wn)[NP], bool (&pd)[NP]) {
+// log det accumulator: det = mant * 2^expo, renormalised every 16 pivots (pivots of a PD test are
+// positive; only PD probes' values are used).
+struct LogDet {
+  double mant;
+  int expo;
+  PSB_HD void init() { mant = 1.0; expo = 0; }
+  // exponent renormalisation with integer ops only (the FP64 pipe is the engine's bottleneck);
+  // a product that left the normal range (only possible for |entries| ~ 1e30+) poisons the value
+  PSB_HD void norm() {
+#ifdef __CUDA_ARCH__
+    const long long b = __double_as_longlong(mant);
+    const int e = (int)((b >> 52) & 0x7ff);
+    if (e == 0 || e == 0x7ff) { mant = __longlong_as_double(0x7ff8000000000000ll); return; }
+    expo += e - 1023;
+    mant = __longlong_as_double((b & ~(0x7ffll << 52)) | (1023ll << 52));
+#else
+    int e;
+    mant = frexp(mant, &e);
+    expo += e;
+#endif
+  }
+  PSB_HD double value() const { return log(mant) + 0.6931471805599453 * expo; }
+};
+
+template <int KLM, int KUM, int NP, bool LD = true>
+PSB_HD void pdw_step(PDWin<KLM, KUM> (&Wn)[NP], bool (&pd)[NP], LogDet (&ld)[NP]) {
   constexpr int B = KLM + KUM;
 #pragma unroll
   for (int q = 0; q < NP; q++) {
     auto& W = Wn[q].W;
     const double dj = W[0][0].x;
     pd[q] = pd[q] && (dj > 0.0);
+    if (LD) ld[q].mant *= dj;
     const double iD = fast_rcp(dj);
     double2 l[B + 1];
 #pragma unroll
@@ -566,11 +591,16 @@ PSB_HD void pdw_test(int n, const double2* __restrict__ Ab, const double2* __res
   double zz[NP];
 #pragma unroll
   for (int q = 0; q < NP; q++) { zz[q] = cnorm2(z) - lam[q]; pd[q] = true; }
+  LogDet ld[NP];
+#pragma unroll
+  for (int q = 0; q < NP; q++) ld[q].init();
 #pragma unroll
   for (int r = 0; r <= B; r++) pdw_load_row<KLM, KUM, NP>(Wn, r, n, r, Ab, AHA, z, zz);
   for (int j = 0; j < n; j++) {
-    pdw_step<KLM, KUM, NP>(Wn, pd);
+    pdw_step<KLM, KUM, NP>(Wn, pd, ld);
     pdw_load_row<KLM, KUM, NP>(Wn, B, n, j + 1 + B, Ab, AHA, z, zz);
+    if ((j & 15) == 15)
+      for (int q = 0; q < NP; q++) ld[q].norm();
   }
 }
 

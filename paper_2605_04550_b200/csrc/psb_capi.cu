@@ -90,12 +90,14 @@ static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 2, 2, 1), K
                                KP(4, 4, 1, 1), KP(1, 2, 2, 1), KP(2, 1, 2, 1)};
 static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,
                            &k_lanczos<16, 16, true, 2>, 0, 1, 1};
-static const KPair kAlt[] = {KP(1, 3, 1, 1), KP(1, 3, 1, 2), KP(1, 3, 3, 1), KP(2, 3, 2, 1), KP(3, 3, 2, 1)};
+#define KPD(KL, KU, NP, G, D)                                                                     \
+  {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, D>, \
+   4 * Ring<KL, KU, D>::BYTES, NP, G}
+static const KPair kD4[] = {KPD(1, 1, 2, 1, 4), KPD(1, 3, 2, 1, 4), KPD(2, 3, 1, 1, 4), KPD(3, 3, 1, 1, 4)};
 static KPair pick(int kl, int ku) {
-  if (getenv("PSB_ALT")) {  // development A/B of the (NP, G) choice
-    const int v = atoi(getenv("PSB_ALT"));
-    for (const KPair& k : kAlt)
-      if (k.kl == kl && k.ku == ku && (v == k.np * 10 + k.g)) return k;
+  if (getenv("PSB_D4")) {  // development A/B of the Lanczos ring depth
+    for (const KPair& k : kD4)
+      if (k.kl == kl && k.ku == ku) return k;
   }
   for (const KPair& k : kTable)
     if (k.kl == kl && k.ku == ku) return k;
@@ -278,6 +280,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.listA = h->listA.as<int64_t>(); ba.listB = h->listB.as<int64_t>(); ba.counters = cnt;
   ba.dyn_L = nullptr; ba.dyn_D = nullptr;
   ba.mode = 0;
+  ba.secant = getenv("PSB_NOSEC") ? 0 : 1;
   const int64_t gridC = std::max<int64_t>(1, std::min<int64_t>((int64_t)occB * h->num_sms, (P + 127) / 128));
   int64_t gridB = (int64_t)occB * h->num_sms;
   if (dyn) {

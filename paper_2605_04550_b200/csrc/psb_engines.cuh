@@ -26,6 +26,7 @@ struct BisArgs {
   int64_t* listB;                 // points the bisection engine owns (mode 1 input)
   unsigned long long* counters;   // [0] work, [1] nA, [2] pd tests, [3] nB done, [7] nB listed
   int mode;                       // 0: classify (one test, split into listA/listB); 1: bisect listB
+  int secant;                     // 1: secant-accelerated multisection (G == 1, NP == 2 shapes)
   double2* dyn_L;                 // DYN only: per-thread b*b ring
   double* dyn_D;                  // DYN only: per-thread 2b
 };
@@ -274,6 +275,7 @@ template <int KL, int KU, bool DYN, int NP, int G>
 __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   constexpr int B = KL + KU;
   constexpr int K = NP * G;
+  constexpr bool SEC = (G == 1 && NP == 2);  // secant acceleration needs two probes per lane
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;               // lane within the group
@@ -283,6 +285,9 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   double2 z = czero();
   double lo = 0.0, hi = 0.0;
   int phase = 1, rounds = 0;
+  // secant acceleration state (G == 1): log det at lo and at the previous PD point lp
+  double Llo = 0.0, lp = 0.0, Lp = 0.0;
+  bool have_lo = false, have_p = false, use_sec = false;
   bool exhausted = false;
   const int64_t total = (a.mode == 0) ? a.P : (int64_t)a.counters[7];
   while (true) {
@@ -312,6 +317,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
             p = pt;
             rounds = 0;
             lo = lam_tau; hi = INFINITY; phase = 1;
+            have_lo = have_p = use_sec = false;
             if (a.mode == 1 && forced) { lo = 0.0; hi = lam_tau; phase = 2; }
           }
         }
@@ -333,10 +339,29 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       else lam[q] = lo + (hi - lo) * (double)(i + 1) / (double)(K + 1);
       if (!me) lam[q] = 1.0;
     }
+    // Secant step (G == 1, NP == 2): det G(lambda) = prod (sigma_i^2 - lambda) is positive, decreasing
+    // and convex below sigma_min^2, so the secant through two PD points (lp, lo) has its root ls below
+    // sigma_min^2 (a valid lower bound). Probe ls and ls + (ls - lo)/10; the PD tests alone decide
+    // the bracket, so a poor secant costs time, never correctness.
+    if constexpr (SEC) {
+      if (a.mode == 1 && me && phase == 2 && use_sec && have_lo && have_p && a.secant) {
+        const double dL = Lp - Llo;  // log(f(lp) / f(lo)) > 0 (NaN if a product overflowed)
+        if (dL > 1e-300 && dL < 700.0) {
+          const double ls = lo + (lo - lp) / expm1(dL);
+          if (ls > lo && ls < hi) {
+            lam[0] = ls;
+            double p1 = ls + 0.1 * (ls - lo);
+            if (!(p1 < hi)) p1 = 0.5 * (ls + hi);
+            lam[1] = p1;
+          }
+        }
+      }
+    }
     const double2 zt = me ? z : czero();
     bool pd[NP];
+    LogDet ld[NP];
 #pragma unroll
-    for (int q = 0; q < NP; q++) pd[q] = true;
+    for (int q = 0; q < NP; q++) { pd[q] = true; ld[q].init(); }
     if constexpr (DYN) {
       const int b = a.kl + a.ku;
       LV Ls{a.dyn_L + tid * (int64_t)(b * b > 0 ? b * b : 1), 1};
@@ -351,16 +376,46 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       for (int q = 0; q < NP; q++) zz[q] = cnorm2(zt) - lam[q];
 #pragma unroll
       for (int r = 0; r <= B; r++) pdw_load_row<KL, KU, NP>(Wn, r, a.n, r, a.Ab, a.AHA, zt, zz);
+      if constexpr (!SEC) {
 #pragma unroll 4
-      for (int j = 0; j < a.n; j++) {
-        pdw_step<KL, KU, NP>(Wn, pd);
-        pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + 1 + B, a.Ab, a.AHA, zt, zz);
-        if ((j & 31) == 31) {
+        for (int j = 0; j < a.n; j++) {
+          pdw_step<KL, KU, NP, false>(Wn, pd, ld);
+          pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + 1 + B, a.Ab, a.AHA, zt, zz);
+          if ((j & 31) == 31) {
+            bool any = false;
+#pragma unroll
+            for (int q = 0; q < NP; q++) any = any || pd[q];
+            if (!__any_sync(FULL, any && me)) break;  // every probe of every active lane failed
+          }
+        }
+      } else {
+      // 8-row blocks without branches inside (log-det renormalisation and the early-exit vote
+      // between blocks), then the remainder rows
+      const int nb = a.n & ~7;
+      int j = 0;
+      for (; j < nb; j += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+          pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + u + 1 + B, a.Ab, a.AHA, zt, zz);
+        }
+        if constexpr (SEC) {
+#pragma unroll
+          for (int q = 0; q < NP; q++) ld[q].norm();
+        }
+        if ((j & 31) == 24) {
           bool any = false;
 #pragma unroll
           for (int q = 0; q < NP; q++) any = any || pd[q];
           if (!__any_sync(FULL, any && me)) break;  // every probe of every active lane failed
         }
+      }
+      if (j >= nb) {
+        for (; j < a.n; j++) {
+          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+          pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + 1 + B, a.Ab, a.AHA, zt, zz);
+        }
+      }
       }
     }
     if (a.mode == 0) {
@@ -398,6 +453,21 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       rounds++;
       int r = BIS_CONTINUE;
       const double nlo = fmax(lo, plo), nhi = fmin(hi, phi);
+      if constexpr (SEC) {
+        // secant bookkeeping: keep the two highest PD points that carry a log det
+        const double old_w = hi - lo;
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+          if (pd[q] && lam[q] > lo) {
+            const double Lq = ld[q].value();
+            if (have_lo) { lp = lo; Lp = Llo; have_p = true; }
+            lo = lam[q]; Llo = Lq; have_lo = true;  // probes are ascending, so lo ends at the top PD one
+          }
+        }
+        lo = fmax(lo, nlo);
+        const double new_w = nhi - lo;
+        use_sec = (phase == 2 || phi < INFINITY) && !(new_w > old_w / 3.0);  // keep going while it pays
+      }
       if (phase == 1 && phi == INFINITY) {
         lo = nlo;  // every probe PD: keep searching upward
       } else {
