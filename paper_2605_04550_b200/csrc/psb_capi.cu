@@ -86,7 +86,7 @@ constexpr int kDepth = 8;  // cp.async ring depth of the Lanczos sweeps (rows in
 #define KP(KL, KU, NP, G)                                                                               \
   {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, kDepth>, \
    4 * Ring<KL, KU, kDepth>::BYTES, NP, G}
-static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 2, 2, 1), KP(2, 3, 1, 1), KP(3, 3, 1, 1),
+static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 2, 2, 1), KP(2, 3, 2, 1), KP(3, 3, 2, 1),
                                KP(4, 4, 1, 1), KP(1, 2, 2, 1), KP(2, 1, 2, 1)};
 static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,
                            &k_lanczos<16, 16, true, 2>, 0, 1, 1};
@@ -94,7 +94,12 @@ static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 
   {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, D>, \
    4 * Ring<KL, KU, D>::BYTES, NP, G}
 static const KPair kD4[] = {KPD(1, 1, 2, 1, 4), KPD(1, 3, 2, 1, 4), KPD(2, 3, 1, 1, 4), KPD(3, 3, 1, 1, 4)};
+static const KPair kNP2[] = {KP(2, 3, 2, 1), KP(3, 3, 2, 1)};
 static KPair pick(int kl, int ku) {
+  if (getenv("PSB_NP2")) {  // development A/B: two probes (+ secant) for the wide shapes
+    for (const KPair& k : kNP2)
+      if (k.kl == kl && k.ku == ku) return k;
+  }
   if (getenv("PSB_D4")) {  // development A/B of the Lanczos ring depth
     for (const KPair& k : kD4)
       if (k.kl == kl && k.ku == ku) return k;
