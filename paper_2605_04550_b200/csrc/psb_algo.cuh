@@ -329,7 +329,7 @@ PSB_HD void sweep_s3(const Shape& s, LV F, LVb piv, LV T, double scale) {  // F 
 // S4: backward sweep, x = U^{-1} (scale * T) with U = D U' (x_j = b_j rinv_j - sum U'_{j,c} x_{j+c}),
 // in place; returns sum_j Re(conj(RA_j) x_j) (the Lanczos alpha numerator).
 template <int KLM, int KUM, bool DYN>
-PSB_HD double sweep_s4(const Shape& s, LV F, LV T, LV RA, double scale) {  // F = FU
+PSB_HD double sweep_s4(const Shape& s, LV F, LV T, LV RA, double scale, double* wn2) {  // F = FU
   constexpr int WM = KLM + KUM;
   const int n = s.n;
   const int W = DYN ? s.W : WM;
@@ -337,7 +337,7 @@ PSB_HD double sweep_s4(const Shape& s, LV F, LV T, LV RA, double scale) {  // F 
   double2 xw[WM + 1];  // xw[c] = x_{j+c}
 #pragma unroll
   for (int c = 0; c <= WM; c++) xw[c] = czero();
-  double acc = 0.0;
+  double acc = 0.0, nn = 0.0;
   for (int j = n - 1; j >= 0; j--) {
     const int64_t rb = (int64_t)j * NF;
     double2 x = cmul(cscale(T.get(j), scale), F.get(rb + W));
@@ -346,10 +346,12 @@ PSB_HD double sweep_s4(const Shape& s, LV F, LV T, LV RA, double scale) {  // F 
       if (c <= W) x = cfms(x, F.get(rb + c - 1), xw[c]);
     T.put(j, x);
     acc += cdotr(RA.get(j), x);
+    nn += cnorm2(x);
 #pragma unroll
     for (int c = WM; c >= 2; c--) xw[c] = xw[c - 1];
     xw[1] = x;
   }
+  *wn2 = nn;
   return acc;
 }
 

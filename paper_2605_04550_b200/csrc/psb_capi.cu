@@ -93,7 +93,8 @@ static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 
 #define KPD(KL, KU, NP, G, D)                                                                     \
   {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, D>, \
    4 * Ring<KL, KU, D>::BYTES, NP, G}
-static const KPair kD4[] = {KPD(1, 1, 2, 1, 4), KPD(1, 3, 2, 1, 4), KPD(2, 3, 1, 1, 4), KPD(3, 3, 1, 1, 4)};
+static const KPair kD4[] = {KPD(1, 1, 2, 1, 4), KPD(1, 3, 2, 1, 4), KPD(2, 3, 2, 1, 4), KPD(3, 3, 2, 1, 4)};
+static const KPair kD6[] = {KPD(1, 1, 2, 1, 6), KPD(1, 3, 2, 1, 6), KPD(2, 3, 2, 1, 6), KPD(3, 3, 2, 1, 6)};
 static const KPair kNP2[] = {KP(2, 3, 2, 1), KP(3, 3, 2, 1)};
 static KPair pick(int kl, int ku) {
   if (getenv("PSB_NP2")) {  // development A/B: two probes (+ secant) for the wide shapes
@@ -102,6 +103,10 @@ static KPair pick(int kl, int ku) {
   }
   if (getenv("PSB_D4")) {  // development A/B of the Lanczos ring depth
     for (const KPair& k : kD4)
+      if (k.kl == kl && k.ku == ku) return k;
+  }
+  if (getenv("PSB_D6")) {
+    for (const KPair& k : kD6)
       if (k.kl == kl && k.ku == ku) return k;
   }
   for (const KPair& k : kTable)

@@ -221,7 +221,7 @@ __device__ void pl_s3(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T, dou
 // S4 (backward): x = U^{-1}(scale*T) in place; returns sum Re(conj(RA_j) x_j).
 // Slot (step q, row j = n-1-q): FU_j | T_j RA_j.
 template <int KL, int KU, int D>
-__device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, double scale) {
+__device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, double scale, double* wn2) {
   typedef Ring<KL, KU, D> RG;
   constexpr int W = RG::W, NU = RG::NU;
   auto issue = [&](int q) {
@@ -238,7 +238,7 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
   double2 xw[W + 1];
 #pragma unroll
   for (int c = 0; c <= W; c++) xw[c] = czero();
-  double acc = 0.0;
+  double acc = 0.0, nn = 0.0;
 #pragma unroll
   for (int q = 0; q < D - 1; q++) issue(q);
 #pragma unroll 2
@@ -252,11 +252,13 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
     for (int c = W; c >= 1; c--) x = cfms(x, *R.at(sl, c - 1), xw[c]);
     T.put(j, x);
     acc += cdotr(*R.at(sl, NU + 1), x);
+    nn += cnorm2(x);
 #pragma unroll
     for (int c = W; c >= 2; c--) xw[c] = xw[c - 1];
     xw[1] = x;
   }
   cp_wait<0>();
+  *wn2 = nn;
   return acc;
 }
 
@@ -612,14 +614,14 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       }
     }
     if (phase == 2) {
-      double acc;
+      double acc, wn2 = 0.0;
       if constexpr (DYN) {
         sweep_s3<KL, KU, DYN>(s, FL, piv, T, 1.0 / (nu * b1));
-        acc = sweep_s4<KL, KU, DYN>(s, FU, T, RA, 1.0 / nu);
+        acc = sweep_s4<KL, KU, DYN>(s, FU, T, RA, 1.0 / nu, &wn2);
       } else {
         pl_s3<KL, KU, DPIPE>(n, ring, FL, piv, T, 1.0 / (nu * b1));
         if (a.prof) { long long t = clock64(); if (lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[3], (unsigned long long)(t - tq1)); tq1 = t; }
-        acc = pl_s4<KL, KU, DPIPE>(n, ring, FU, T, RA, 1.0 / nu);
+        acc = pl_s4<KL, KU, DPIPE>(n, ring, FU, T, RA, 1.0 / nu, &wn2);
         if (a.prof) { long long t = clock64(); if (lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[4], (unsigned long long)(t - tq1)); tq1 = t; }
       }
       const double alpha = acc / b1;
@@ -635,6 +637,17 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       theta = th;
       s2 = sq;
       aprev = alpha;
+      // Early convergence test (saves the next S1 sweep): with v_k orthogonal to v_{k-1},
+      // ||r_{k+1}||^2 = ||w||^2 - alpha_k^2 - beta_{k-1}^2. Cancellation makes that estimate
+      // unreliable exactly when beta_k << ||w||, so use the certified upper bound
+      // beta_up = sqrt(max(est, 0) + 4 n eps ||w||^2); r_up = beta_up |s_k| >= the true residual.
+      if (k >= 2) {
+        const double est = wn2 - alpha * alpha - b1 * b1;
+        const double beta_up = sqrt(fmax(est, 0.0) + 4.0 * n * 2.220446049250313e-16 * wn2);
+        const double r_up = beta_up * sqrt(fmax(s2, 0.0));
+        if (isfinite(theta) && theta > 0.0 && lanczos_converged(theta, dth, r_up, beta_up))
+          finish(1.0 / (nu * sqrt(theta)), k, 0);
+      }
       k++;
     }
   }
