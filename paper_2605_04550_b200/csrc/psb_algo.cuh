@@ -556,6 +556,21 @@ struct LogDet {
   PSB_HD double value() const { return log(mant) + 0.6931471805599453 * expo; }
 };
 
+// Same as pdw_load_row with the G row entries given (rows of a diagonal-constant band share them).
+template <int KLM, int KUM, int NP>
+PSB_HD void pdw_load_row_g(PDWin<KLM, KUM> (&Wn)[NP], int r, const double2 (&g)[KLM + KUM + 1],
+                           const double (&zz)[NP]) {
+  constexpr int B = KLM + KUM;
+#pragma unroll
+  for (int q = 0; q < NP; q++) {
+#pragma unroll
+    for (int c = 0; c <= B; c++)
+      if (c <= r) Wn[q].W[r][c] = g[r - c];
+    Wn[q].W[r][r].x += zz[q];
+    Wn[q].W[r][r].y = 0.0;
+  }
+}
+
 template <int KLM, int KUM, int NP, bool LD = true>
 PSB_HD void pdw_step(PDWin<KLM, KUM> (&Wn)[NP], bool (&pd)[NP], LogDet (&ld)[NP]) {
   constexpr int B = KLM + KUM;

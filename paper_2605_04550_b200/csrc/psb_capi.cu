@@ -51,6 +51,7 @@ struct psb_handle {
   // matrix
   int n = 0, kl = 0, ku = 0;
   double anorm = 0.0;
+  int tz_j0 = 1, tz_j1 = 0;  // interior rows sharing one G row (diagonal-constant band), empty by default
   bool have_matrix = false;
   DevBuf Ab, AHA, v1;
   // per call
@@ -226,17 +227,40 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
   CK(cudaStreamSynchronize(h->stream));
   h->n = n; h->kl = kl; h->ku = ku;
   h->anorm = std::sqrt(n1 * ni);
+  // Rows whose G(lambda) row entries are bitwise identical (every band diagonal constant there and
+  // all terms of A^H A present): the bisection engine forms that row once per test. The values are
+  // the same numbers the per-row path would load, so results do not change.
+  {
+    auto same_row = [&](int i, int m) {
+      for (int d = 0; d <= b; d++) {
+        if (aha[(size_t)d * n + i] != aha[(size_t)d * n + m]) return false;
+        if (d <= kl && A[(int64_t)(kl - d) * n + i] != A[(int64_t)(kl - d) * n + m]) return false;
+        if (d <= ku && A[(int64_t)(kl + d) * n + (i - d)] != A[(int64_t)(kl + d) * n + (m - d)]) return false;
+      }
+      return true;
+    };
+    const int m = n / 2;
+    h->tz_j0 = 1; h->tz_j1 = 0;
+    if (m >= b && m + kl < n) {
+      int j0 = m, j1 = m;
+      while (j0 - 1 >= b && same_row(j0 - 1, m)) j0--;
+      while (j1 + 1 + kl < n && same_row(j1 + 1, m)) j1++;
+      if (j1 - j0 >= 16) { h->tz_j0 = j0; h->tz_j1 = j1; }
+    }
+  }
   h->have_matrix = true;
   return PSB_OK;
 }
 
 }  // extern "C"
 
-// Flop / byte models: per row of one PD test and of one Lanczos step.
-static double flops_pd_row(int kl, int ku) {
-  const int b = kl + ku;
-  return 8.0 * (kl + 1) + 8.0 * (ku + 1) + 2.0 + 8.0 * b * (b - 1) / 2.0 + 4.0 * b + 4.0 * b + 1.0;
-}
+// Flop / byte models, counting only the arithmetic the kernels must do.
+// One right-looking LDL^H row per probe: b column scalings (2 flops), b(b-1)/2 off-diagonal complex
+// updates (8), b diagonal updates (4), one reciprocal (1) -> 4b^2 + 2b + 1.
+static double flops_ldl_row(int kl, int ku) { const double b = kl + ku; return 4.0 * b * b + 2.0 * b + 1.0; }
+// Forming one G row: b+1 entries AHA - conj(z) A_low - z conj(A_up) (+ the diagonal shift); shared by
+// the probes of a round, and formed once per round for the interior rows of a diagonal-constant band.
+static double flops_g_row(int kl, int ku) { return 8.0 * (kl + 1) + 8.0 * (ku + 1) + 2.0; }
 static double flops_lu_row(int kl, int ku) { const int W = kl + ku; return 6.0 * W + 6.0 + kl * (6.0 + 8.0 * W); }
 static double flops_it_row(int kl, int ku) {
   const int W = kl + ku;
@@ -291,6 +315,8 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.dyn_L = nullptr; ba.dyn_D = nullptr;
   ba.mode = 0;
   ba.secant = getenv("PSB_NOSEC") ? 0 : 1;
+  ba.tz_j0 = getenv("PSB_NOTZ") ? 1 : h->tz_j0;
+  ba.tz_j1 = getenv("PSB_NOTZ") ? 0 : h->tz_j1;
   const int64_t gridC = std::max<int64_t>(1, std::min<int64_t>((int64_t)occB * h->num_sms, (P + 127) / 128));
   int64_t gridB = (int64_t)occB * h->num_sms;
   if (dyn) {
@@ -387,7 +413,12 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   S.n_lanczos = (int64_t)hc[6];
   S.pd_tests = (int64_t)hc[2] + nA;  // bisected points count their classification test; + Lanczos points' one
   S.lanczos_iters = (int64_t)hc[5];
-  S.flops_bisect = (double)S.pd_tests * n * flops_pd_row(kl, ku);
+  {
+    const double n_int = (h->tz_j0 <= h->tz_j1) ? (double)(h->tz_j1 - h->tz_j0 + 1) : 0.0;
+    const double g_rows = (double)n - n_int + (n_int > 0 ? 1.0 : 0.0);  // rows that form G per round
+    const double rounds = (double)(int64_t)hc[2] / (double)kp.np + (double)nA + (double)nB;  // + classification
+    S.flops_bisect = (double)S.pd_tests * n * flops_ldl_row(kl, ku) + rounds * g_rows * flops_g_row(kl, ku);
+  }
   S.flops_lanczos = (double)hc[6] * n * flops_lu_row(kl, ku) + (double)hc[5] * n * flops_it_row(kl, ku);
   S.bytes_lanczos = (double)hc[6] * n * (16.0 * (s.NU + kl) + 4.0) + (double)hc[5] * n * bytes_it_row(kl, ku);
   S.ms_bisect = msC + msB; S.ms_lanczos = msL; S.ms_total = msT;

@@ -27,6 +27,7 @@ struct BisArgs {
   unsigned long long* counters;   // [0] work, [1] nA, [2] pd tests, [3] nB done, [7] nB listed
   int mode;                       // 0: classify (one test, split into listA/listB); 1: bisect listB
   int secant;                     // 1: secant-accelerated multisection (G == 1, NP == 2 shapes)
+  int tz_j0, tz_j1;               // rows [tz_j0, tz_j1] share one G row (diagonal-constant band); j0 > j1: none
   double2* dyn_L;                 // DYN only: per-thread b*b ring
   double* dyn_D;                  // DYN only: per-thread 2b
 };
@@ -376,13 +377,22 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       double zz[NP];
 #pragma unroll
       for (int q = 0; q < NP; q++) zz[q] = cnorm2(zt) - lam[q];
+      // interior rows of a diagonal-constant band: the G row is a function of z only
+      double2 gc[B + 1];
+      const bool tz = a.tz_j0 <= a.tz_j1;
+#pragma unroll
+      for (int d = 0; d <= B; d++) gc[d] = tz ? g_entry<KL, KU>(a.n, a.tz_j0, d, a.Ab, a.AHA, zt, 0.0) : czero();
+      auto load_new = [&](int i) {
+        if (tz && i >= a.tz_j0 && i <= a.tz_j1) pdw_load_row_g<KL, KU, NP>(Wn, B, gc, zz);
+        else pdw_load_row<KL, KU, NP>(Wn, B, a.n, i, a.Ab, a.AHA, zt, zz);
+      };
 #pragma unroll
       for (int r = 0; r <= B; r++) pdw_load_row<KL, KU, NP>(Wn, r, a.n, r, a.Ab, a.AHA, zt, zz);
       if constexpr (!SEC) {
 #pragma unroll 4
         for (int j = 0; j < a.n; j++) {
           pdw_step<KL, KU, NP, false>(Wn, pd, ld);
-          pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + 1 + B, a.Ab, a.AHA, zt, zz);
+          load_new(j + 1 + B);
           if ((j & 31) == 31) {
             bool any = false;
 #pragma unroll
@@ -399,7 +409,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
 #pragma unroll
         for (int u = 0; u < 8; u++) {
           pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
-          pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + u + 1 + B, a.Ab, a.AHA, zt, zz);
+          load_new(j + u + 1 + B);
         }
         if constexpr (SEC) {
 #pragma unroll
@@ -415,7 +425,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       if (j >= nb) {
         for (; j < a.n; j++) {
           pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
-          pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + 1 + B, a.Ab, a.AHA, zt, zz);
+          load_new(j + 1 + B);
         }
       }
       }
