@@ -52,6 +52,11 @@ struct psb_handle {
   int n = 0, kl = 0, ku = 0;
   double anorm = 0.0;
   int tz_j0 = 1, tz_j1 = 0;  // interior rows sharing one G row (diagonal-constant band), empty by default
+  // development knobs, read once at psb_create (A/B switches; defaults are the product path):
+  //   PSB_NOSEC=1 plain multisection, PSB_NOTZ=1 per-row G formation, PSB_LWARPS=N cap on
+  //   Lanczos warps, PSB_PROF=1 per-phase clock64 counters of the Lanczos kernel (stderr)
+  bool k_secant = true, k_toeplitz = true, k_prof = false;
+  long long k_lwarps = 0;
   bool have_matrix = false;
   DevBuf Ab, AHA, v1;
   // per call
@@ -91,25 +96,7 @@ static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 2, 2, 1), K
                                KP(4, 4, 1, 1), KP(1, 2, 2, 1), KP(2, 1, 2, 1)};
 static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,
                            &k_lanczos<16, 16, true, 2>, 0, 1, 1};
-#define KPD(KL, KU, NP, G, D)                                                                     \
-  {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, D>, \
-   4 * Ring<KL, KU, D>::BYTES, NP, G}
-static const KPair kD4[] = {KPD(1, 1, 2, 1, 4), KPD(1, 3, 2, 1, 4), KPD(2, 3, 2, 1, 4), KPD(3, 3, 2, 1, 4)};
-static const KPair kD6[] = {KPD(1, 1, 2, 1, 6), KPD(1, 3, 2, 1, 6), KPD(2, 3, 2, 1, 6), KPD(3, 3, 2, 1, 6)};
-static const KPair kNP2[] = {KP(2, 3, 2, 1), KP(3, 3, 2, 1)};
 static KPair pick(int kl, int ku) {
-  if (getenv("PSB_NP2")) {  // development A/B: two probes (+ secant) for the wide shapes
-    for (const KPair& k : kNP2)
-      if (k.kl == kl && k.ku == ku) return k;
-  }
-  if (getenv("PSB_D4")) {  // development A/B of the Lanczos ring depth
-    for (const KPair& k : kD4)
-      if (k.kl == kl && k.ku == ku) return k;
-  }
-  if (getenv("PSB_D6")) {
-    for (const KPair& k : kD6)
-      if (k.kl == kl && k.ku == ku) return k;
-  }
   for (const KPair& k : kTable)
     if (k.kl == kl && k.ku == ku) return k;
   return kDyn;
@@ -132,6 +119,10 @@ int psb_create(int device, psb_handle** out) {
   h->device = device;
   if (cudaSetDevice(device) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  h->k_secant = getenv("PSB_NOSEC") == nullptr;
+  h->k_toeplitz = getenv("PSB_NOTZ") == nullptr;
+  h->k_prof = getenv("PSB_PROF") != nullptr;
+  h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
@@ -314,9 +305,9 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.listA = h->listA.as<int64_t>(); ba.listB = h->listB.as<int64_t>(); ba.counters = cnt;
   ba.dyn_L = nullptr; ba.dyn_D = nullptr;
   ba.mode = 0;
-  ba.secant = getenv("PSB_NOSEC") ? 0 : 1;
-  ba.tz_j0 = getenv("PSB_NOTZ") ? 1 : h->tz_j0;
-  ba.tz_j1 = getenv("PSB_NOTZ") ? 0 : h->tz_j1;
+  ba.secant = h->k_secant ? 1 : 0;
+  ba.tz_j0 = h->k_toeplitz ? h->tz_j0 : 1;
+  ba.tz_j1 = h->k_toeplitz ? h->tz_j1 : 0;
   const int64_t gridC = std::max<int64_t>(1, std::min<int64_t>((int64_t)occB * h->num_sms, (P + 127) / 128));
   int64_t gridB = (int64_t)occB * h->num_sms;
   if (dyn) {
@@ -330,6 +321,10 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   kp.b<<<(unsigned)gridC, 128, 0, st>>>(ba);
   CK(cudaGetLastError());
   CK(cudaEventRecord(h->ev[1], st));
+  // One host round trip reads the list lengths: it sizes both grids and, more importantly, makes the
+  // Lanczos blocks (large shared-memory ring) land on every SM before the bisection blocks are
+  // submitted. (Launching both straight after classification let the bisection engine take two
+  // blocks per SM first and left the Lanczos engine short of SMs: C2 3.3 -> 4.6 ms, measured.)
   unsigned long long hc0[8];
   CK(cudaMemcpyAsync(hc0, cnt, sizeof(hc0), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -350,7 +345,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     const double per_warp = warp_stride * 16.0 + piv_stride * 4.0;
     int64_t warps = std::min<int64_t>((int64_t)occL * h->num_sms * 4, (nA + 31) / 32);
     warps = std::min<int64_t>(warps, (int64_t)(budget / per_warp));
-    if (getenv("PSB_LWARPS")) warps = std::min<int64_t>(warps, atoll(getenv("PSB_LWARPS")));
+    if (h->k_lwarps > 0) warps = std::min<int64_t>(warps, h->k_lwarps);
     warps = std::max<int64_t>(4, (warps + 3) / 4 * 4);
     gridL = warps / 4;
     CK(h->scratch.ensure((size_t)(warps * warp_stride * sizeof(double2))));
@@ -364,7 +359,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     la.warp_stride = warp_stride; la.piv_stride = piv_stride;
     la.kmax = kmax; la.refill = std::min(32, std::max(1, opt.refill));
     la.prof = nullptr;
-    if (getenv("PSB_PROF")) {
+    if (h->k_prof) {
       CK(h->prof.ensure(64));
       CK(cudaMemsetAsync(h->prof.p, 0, 64, st));
       la.prof = h->prof.as<unsigned long long>();
@@ -397,12 +392,13 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   unsigned long long hc[8];
   CK(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  const int64_t nA_run = (int64_t)hc[1], nB_run = (int64_t)hc[7];
   float msC = 0, msB = 0, msL = 0, msT = 0;
   cudaEventElapsedTime(&msC, h->ev[0], h->ev[1]);
   cudaEventElapsedTime(&msB, h->ev[1], h->ev[2]);
   if (nA > 0) cudaEventElapsedTime(&msL, h->ev[1], h->ev[3]);
   cudaEventElapsedTime(&msT, h->ev[0], h->ev[4]);
-  if (getenv("PSB_PROF") && nA > 0) {
+  if (h->k_prof && nA_run > 0) {
     unsigned long long pr[8];
     cudaMemcpy(pr, h->prof.p, 64, cudaMemcpyDeviceToHost);
     fprintf(stderr, "[psb prof] warp-cycles: lu %.3g s1 %.3g s2 %.3g s3 %.3g s4 %.3g ritz %.3g (gridL %lld)\n",
@@ -411,12 +407,12 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   psb_stats& S = h->stats;
   S.n_bisect = (int64_t)hc[3];
   S.n_lanczos = (int64_t)hc[6];
-  S.pd_tests = (int64_t)hc[2] + nA;  // bisected points count their classification test; + Lanczos points' one
+  S.pd_tests = (int64_t)hc[2] + nA_run;  // bisected points count their classification test; + Lanczos points' one
   S.lanczos_iters = (int64_t)hc[5];
   {
     const double n_int = (h->tz_j0 <= h->tz_j1) ? (double)(h->tz_j1 - h->tz_j0 + 1) : 0.0;
     const double g_rows = (double)n - n_int + (n_int > 0 ? 1.0 : 0.0);  // rows that form G per round
-    const double rounds = (double)(int64_t)hc[2] / (double)kp.np + (double)nA + (double)nB;  // + classification
+    const double rounds = (double)(int64_t)hc[2] / (double)kp.np + (double)nA_run + (double)nB_run;  // + classification
     S.flops_bisect = (double)S.pd_tests * n * flops_ldl_row(kl, ku) + rounds * g_rows * flops_g_row(kl, ku);
   }
   S.flops_lanczos = (double)hc[6] * n * flops_lu_row(kl, ku) + (double)hc[5] * n * flops_it_row(kl, ku);
