@@ -86,12 +86,12 @@ static int fail(psb_handle* h, int code, const std::string& msg) {
 typedef void (*bis_fn)(BisArgs);
 typedef void (*lan_fn)(LanArgs);
 // b: classification (NP = 1); bm: multisection (NP probes per thread); l: Lanczos engine.
-struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np, g; };
+struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np, g; };  // lsmem: per warp
 constexpr int kDepth = 8;  // cp.async ring depth of the Lanczos sweeps (rows in flight + 1)
 // (NP probes per lane) x (G lanes per point), fixed per band shape (results must not depend on the batch)
 #define KP(KL, KU, NP, G)                                                                               \
   {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, kDepth>, \
-   4 * Ring<KL, KU, kDepth>::BYTES, NP, G}
+   Ring<KL, KU, kDepth>::BYTES, NP, G}
 static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 2, 2, 1), KP(2, 3, 2, 1), KP(3, 3, 2, 1),
                                KP(4, 4, 1, 1), KP(1, 2, 2, 1), KP(2, 1, 2, 1)};
 static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,
@@ -335,19 +335,24 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   const Shape s = make_shape(n, kl, ku);
   const int64_t warp_stride = ((int64_t)n * (s.NU + s.NL + 3) + kmax) * 32;  // double2 units
   const int64_t piv_stride = ((int64_t)n * 32 + 63) / 64 * 64;                 // int32 units
+  // Engine L runs 4-warp blocks (one block per SM with the 8-deep ring). One-warp blocks spread its
+  // warps over every SM: faster alone (C2 3.0 -> 2.6 ms) but the concurrent step got slower (3.3 ->
+  // 4.3 ms) because every SM then hosts more engine-L warps next to the FP64-bound bisection warps.
+  constexpr int kLWarpsPerBlock = 4;
+  const int lsmem = kp.lsmem * kLWarpsPerBlock;
   int64_t gridL = 0;
   int occL = 0;
   if (nA > 0) {
-    if (kp.lsmem > 48 * 1024) CK(cudaFuncSetAttribute(kp.l, cudaFuncAttributeMaxDynamicSharedMemorySize, kp.lsmem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occL, kp.l, 128, kp.lsmem));
+    if (lsmem > 48 * 1024) CK(cudaFuncSetAttribute(kp.l, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occL, kp.l, 32 * kLWarpsPerBlock, lsmem));
     occL = std::max(occL, 1);
     const double budget = 24.0 * (1ull << 30);  // scratch budget (HBM is 180 GB)
     const double per_warp = warp_stride * 16.0 + piv_stride * 4.0;
-    int64_t warps = std::min<int64_t>((int64_t)occL * h->num_sms * 4, (nA + 31) / 32);
+    int64_t warps = std::min<int64_t>((int64_t)occL * h->num_sms * kLWarpsPerBlock, (nA + 31) / 32);
     warps = std::min<int64_t>(warps, (int64_t)(budget / per_warp));
     if (h->k_lwarps > 0) warps = std::min<int64_t>(warps, h->k_lwarps);
-    warps = std::max<int64_t>(4, (warps + 3) / 4 * 4);
-    gridL = warps / 4;
+    warps = std::max<int64_t>(kLWarpsPerBlock, (warps + kLWarpsPerBlock - 1) / kLWarpsPerBlock * kLWarpsPerBlock);
+    gridL = warps / kLWarpsPerBlock;
     CK(h->scratch.ensure((size_t)(warps * warp_stride * sizeof(double2))));
     CK(h->pivs.ensure((size_t)(warps * piv_stride * 4)));
     LanArgs la;
@@ -366,7 +371,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     }
     CK(cudaEventRecord(h->ev[5], st));
     CK(cudaStreamWaitEvent(h->stream2, h->ev[5], 0));
-    kp.l<<<(unsigned)gridL, 128, kp.lsmem, h->stream2>>>(la);
+    kp.l<<<(unsigned)gridL, 32 * kLWarpsPerBlock, lsmem, h->stream2>>>(la);
     CK(cudaGetLastError());
     CK(cudaEventRecord(h->ev[3], h->stream2));
   }
