@@ -365,7 +365,8 @@ def run_ours(args, rank, world, local_rank):
                                     "flops_per_point": flops_pt},
             "engines": {"lanczos_points": s["n_lanczos"], "bisect_points": s["n_bisect"],
                         "lanczos_steps": s["lanczos_iters"], "pd_tests": s["pd_tests"]},
-            "gpu_launches": 2 * args.steps,
+            # per step: the classification kernel, then engine L and engine B when they have points
+            "gpu_launches": int(sum(1 + (s_["grid_lanczos"] > 0) + (s_["grid_bisect"] > 0) for s_ in stats)),
             "clocks": clocks,
         }
         if cpu:

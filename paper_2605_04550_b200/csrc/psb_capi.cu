@@ -87,11 +87,10 @@ typedef void (*bis_fn)(BisArgs);
 typedef void (*lan_fn)(LanArgs);
 // b: classification (NP = 1); bm: multisection (NP probes per thread); l: Lanczos engine.
 struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np, g; };  // lsmem: per warp
-constexpr int kDepth = 8;  // cp.async ring depth of the Lanczos sweeps (rows in flight + 1)
 // (NP probes per lane) x (G lanes per point), fixed per band shape (results must not depend on the batch)
 #define KP(KL, KU, NP, G)                                                                               \
-  {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, kDepth>, \
-   Ring<KL, KU, kDepth>::BYTES, NP, G}
+  {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, RingDepth<KL, KU>::D>, \
+   Ring<KL, KU, RingDepth<KL, KU>::D>::BYTES, NP, G}
 static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 2, 2, 1), KP(2, 3, 2, 1), KP(3, 3, 2, 1),
                                KP(4, 4, 1, 1), KP(1, 2, 2, 1), KP(2, 1, 2, 1)};
 static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,

@@ -263,6 +263,13 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
   return acc;
 }
 
+// cp.async ring depth (rows in flight + 1): 16 for tridiagonal bands, 8 otherwise. Measured on
+// B200: C4 (1,1) 425 -> 400 ms at 16; C2 (1,3) 3.26 -> 3.45 ms at 13, so wider bands keep 8.
+template <int KL, int KU>
+struct RingDepth {
+  static constexpr int D = (KL + KU <= 2) ? 16 : 8;
+};
+
 __device__ __forceinline__ int64_t out_index(const int64_t* outidx, int64_t p) { return outidx ? outidx[p] : p; }
 
 // ----------------------------------------------------------------- engine B kernel
