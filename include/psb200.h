@@ -16,6 +16,9 @@
  *   psb_predict_points    <- pseudospec/pipeline.py:169-172 _predict_points (+ features.py:129-164,
  *                            network.py:62-92,153-190)
  *   psb_region_select     <- pseudospec/pipeline.py:227-231 predicted_region (+ core.py:224-231 dilate)
+ *   psb_recall_sweep      <- pseudospec/pipeline.py:258-259 the calibrate_threshold tau loop
+ *   psb_write_field_csv   <- pseudospec/io.py:92-102 write_field_csv (host only, no handle)
+ *   psb_write_mask_csv    <- pseudospec/io.py:105-115 write_mask_csv (host only, no handle)
  *
  * Conventions (mirroring the reference):
  *   - complex values are interleaved (re, im) float64 pairs, i.e. numpy complex128 memory;
@@ -39,6 +42,7 @@ extern "C" {
 #define PSB_ERR_PARAM 1
 #define PSB_ERR_NUMERICAL 2
 #define PSB_ERR_CUDA 3
+#define PSB_ERR_IO 4 /* file could not be opened or written (the writers below) */
 
 typedef struct psb_handle psb_handle;
 
@@ -112,6 +116,23 @@ int psb_predict_points(psb_handle* h, const double* params, const double* mean33
  * plus the row-major compacted index list of selected points (idx int64[ny*nx], *count). */
 int psb_region_select(psb_handle* h, const double* prob, int32_t ny, int32_t nx, double tau, int32_t k,
                       uint8_t* region, int64_t* idx, int64_t* count);
+
+/* calibrate_threshold's inner loop (pipeline.py:258-259, _recall pipeline.py:234-238): for each
+ * taus[t], recall[t] = |dilate(prob >= taus[t], k) & truth| / |truth| (1.0 when truth is empty).
+ * prob float64[ny*nx]; truth uint8[ny*nx] (the 3x3-dilated exact zone); n_tau <= 4096. */
+int psb_recall_sweep(psb_handle* h, const double* prob, const uint8_t* truth, int32_t ny, int32_t nx, int32_t k,
+                     const double* taus, int32_t n_tau, double* recall);
+
+/* ---- field / mask export (host only; no handle, no GPU) ----
+ * Byte-identical to the reference writers: header line, then one row per grid point in
+ * row-major order (i over ys, j over xs), every float as Python's f"{v:.17g}" ("nan", "inf",
+ * "-inf" for the special values). log10_sigma is float64[ny*nx] = numpy log10 of the field
+ * (computed by the caller, as io.py:97-98); mask is uint8[ny*nx], 0 or 1. nthreads <= 0: all
+ * hardware threads. Returns PSB_OK, PSB_ERR_PARAM or PSB_ERR_IO. */
+int psb_write_field_csv(const char* path, const double* xs, int64_t nx, const double* ys, int64_t ny,
+                        const double* log10_sigma, int32_t nthreads);
+int psb_write_mask_csv(const char* path, const double* xs, int64_t nx, const double* ys, int64_t ny,
+                       const uint8_t* mask, int32_t nthreads);
 
 #ifdef __cplusplus
 }

@@ -9,7 +9,10 @@ The guided-path fixtures (K2) come from the reference's pipeline.hierarchical_pr
 predicted_region with a bundle trained *by the reference* (network.train, calibrate_threshold)
 on a seeded Grcar-family corpus (see train_grcar_bundle).
 
-Usage:  python oracle/make_golden.py sigma|model|guided|all
+The writer fixtures (io) are the reference's own io.write_field_csv / write_mask_csv bytes; the
+calibration fixture (calib) is the reference's calibrate_threshold on a small validation corpus.
+
+Usage:  python oracle/make_golden.py sigma|model|guided|io|calib|all
 """
 
 from __future__ import annotations
@@ -215,6 +218,62 @@ def gen_guided():
     print("c1 guided evals", ne1, "region frac", reg1.mean(), flush=True)
 
 
+def special_field_values():
+    """A 6x7 field covering the writer's special cases (exact 0 -> -inf, NaN, inf, subnormal,
+    extremes, values needing all 17 digits)."""
+    v = np.array([0.0, np.nan, np.inf, 5e-324, 1e-320, 2.2250738585072014e-308, 1e-300, 1e-5, 1e-4, 0.1, 1.0,
+                  1.0000000000000002, 3.141592653589793, 10.0, 100.0, 1e15, 1e16, 1e17, 1.2345678901234567e21,
+                  1.7976931348623157e308, 0.30000000000000004, 2.5, 1e22, 9.999999999999999e22, 123456.789,
+                  7.0e-5, 6.02214076e23, 1.6e-19, 0.5, 0.25, 0.125, 4.9406564584124654e-324, 1e-7,
+                  0.9999999999999999, 12.0, 1e5, 65504.0, 3e-3, 2.0 ** -40, 2.0 ** 60, 7.77e-7, 42.0])
+    return v.reshape(6, 7)
+
+
+def gen_io():
+    import hashlib
+    import tempfile
+    from pseudospec import io as rio
+    from pseudospec.core import SigmaField, make_grid
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        demo = np.load(GOLD / "demo01_field.npz")["values"]
+        g = make_grid(-1.5, 1.5, -1.5, 1.5, 120, 120)
+        rio.write_field_csv(f"{td}/demo.csv", SigmaField(g, demo))
+        data = open(f"{td}/demo.csv", "rb").read()
+        shipped = Path("/root/reference/pkg/demos/output_01_field.csv").read_bytes()
+        out["demo01_sha256"] = np.array(hashlib.sha256(data).hexdigest())
+        out["demo01_matches_shipped"] = np.array(data == shipped)
+        gs = make_grid(-2.0, 7.5, -0.3, 1e-3, 7, 6)
+        rio.write_field_csv(f"{td}/special.csv", SigmaField(gs, special_field_values()))
+        out["special_csv"] = np.frombuffer(open(f"{td}/special.csv", "rb").read(), dtype=np.uint8)
+        rng = np.random.default_rng(5)
+        mask = rng.random((9, 11)) < 0.4
+        gm = make_grid(-1.0, 3.0, -3.5, 3.5, 11, 9)
+        rio.write_mask_csv(f"{td}/mask.csv", mask, gm)
+        out["mask"] = mask
+        out["mask_csv"] = np.frombuffer(open(f"{td}/mask.csv", "rb").read(), dtype=np.uint8)
+    np.savez_compressed(GOLD / "io_writers.npz", **out)
+    print("io: demo01 matches shipped", bool(out["demo01_matches_shipped"]), flush=True)
+
+
+def gen_calib():
+    from pseudospec import calibrate_threshold, make_grid
+    bundle = load_bundle_npz()
+    grid = make_grid(-1, 3, -3.5, 3.5, 48, 48)
+    va = grcar_family(4, seed=7002)
+    with threadpool_limits(1):
+        rep = calibrate_threshold(bundle, va, grid, 0.01, workers=1)
+    mats = np.empty(len(va), dtype=object)
+    for i, e in enumerate(va):
+        mats[i] = e.matrix
+    np.savez_compressed(GOLD / "calib_grcar.npz", recalls=rep.recalls, median=rep.median_recall,
+                        p10=rep.p10_recall, tau_star=np.array(np.nan if rep.tau_star is None else rep.tau_star),
+                        passed=np.array(rep.passed), probe_seeds=np.array([e.probe_seed for e in va]),
+                        indices=np.array([e.index for e in va]),
+                        **{f"matrix_{i}": e.matrix for i, e in enumerate(va)})
+    print("calib: passed", rep.passed, rep.tau_star, flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("sigma", "all"):
@@ -225,3 +284,7 @@ if __name__ == "__main__":
         train_grcar_bundle()
     if what in ("guided", "all"):
         gen_guided()
+    if what in ("io", "all"):
+        gen_io()
+    if what in ("calib", "all"):
+        gen_calib()

@@ -19,13 +19,14 @@ import numpy as np
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("PSB200_LIB", _HERE / "libpsb200.so"))
 
-PSB_OK, PSB_ERR_PARAM, PSB_ERR_NUMERICAL, PSB_ERR_CUDA = 0, 1, 2, 3
+PSB_OK, PSB_ERR_PARAM, PSB_ERR_NUMERICAL, PSB_ERR_CUDA, PSB_ERR_IO = 0, 1, 2, 3, 4
 
 #: every symbol include/psb200.h declares (checked by the CPU test-suite)
 EXPORTS = (
     "psb_create", "psb_destroy", "psb_last_error", "psb_version", "psb_set_matrix",
     "psb_smin_points", "psb_smin_grid", "psb_smin_points_device", "psb_get_stats",
-    "psb_predict_points", "psb_region_select", "psb_fp64_peak",
+    "psb_predict_points", "psb_region_select", "psb_fp64_peak", "psb_recall_sweep",
+    "psb_write_field_csv", "psb_write_mask_csv",
 )
 
 
@@ -80,6 +81,9 @@ def load_library(path: Path | str | None = None) -> C.CDLL:
         lib.psb_smin_points_device.argtypes = [_P, _P, C.c_int64, C.POINTER(Opts), _P, _P, _P, _P]
         lib.psb_get_stats.argtypes = [_P, C.POINTER(Stats)]
         lib.psb_fp64_peak.argtypes = [_P, C.POINTER(C.c_double)]
+        lib.psb_recall_sweep.argtypes = [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, _P]
+        lib.psb_write_field_csv.argtypes = [C.c_char_p, _P, C.c_int64, _P, C.c_int64, _P, C.c_int32]
+        lib.psb_write_mask_csv.argtypes = [C.c_char_p, _P, C.c_int64, _P, C.c_int64, _P, C.c_int32]
         lib.psb_predict_points.argtypes = [_P, _P, _P, _P, _P, _P, C.c_int32, _P, _P, C.c_int64, _P]
         lib.psb_region_select.argtypes = [_P, _P, C.c_int32, C.c_int32, C.c_double, C.c_int32, _P, _P,
                                           C.POINTER(C.c_int64)]

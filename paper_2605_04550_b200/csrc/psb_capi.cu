@@ -654,4 +654,39 @@ int psb_region_select(psb_handle* h, const double* prob, int32_t ny, int32_t nx,
   return PSB_OK;
 }
 
+int psb_recall_sweep(psb_handle* h, const double* prob, const uint8_t* truth, int32_t ny, int32_t nx, int32_t k,
+                     const double* taus, int32_t n_tau, double* recall) {
+  if (!h) return PSB_ERR_PARAM;
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (!prob || !truth || !taus || !recall || ny < 1 || nx < 1 || k < 1 || (k % 2) == 0 || n_tau < 1 ||
+      n_tau > 4096)
+    return fail(h, PSB_ERR_PARAM, "bad recall-sweep arguments");
+  const int64_t N = (int64_t)ny * nx;
+  int64_t denom = 0;
+  for (int64_t g = 0; g < N; g++) denom += truth[g] ? 1 : 0;
+  if (denom == 0) {  // _recall: an empty truth zone has recall 1.0 (pipeline.py:235-237)
+    for (int t = 0; t < n_tau; t++) recall[t] = 1.0;
+    return PSB_OK;
+  }
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  CK(h->prob.ensure(sizeof(double) * N));
+  CK(h->region.ensure(N));
+  CK(h->xs.ensure(sizeof(double) * n_tau + sizeof(unsigned long long) * n_tau));
+  double* d_taus = h->xs.as<double>();
+  unsigned long long* d_cnt = reinterpret_cast<unsigned long long*>(d_taus + n_tau);
+  CK(cudaMemcpyAsync(h->prob.p, prob, sizeof(double) * N, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(h->region.p, truth, N, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_taus, taus, sizeof(double) * n_tau, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * n_tau, st));
+  k_recall<<<(unsigned)((N + 255) / 256), 256, sizeof(unsigned) * n_tau, st>>>(
+      h->prob.as<double>(), h->region.as<uint8_t>(), ny, nx, k, d_taus, n_tau, d_cnt);
+  CK(cudaGetLastError());
+  std::vector<unsigned long long> cnt((size_t)n_tau);
+  CK(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(unsigned long long) * n_tau, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int t = 0; t < n_tau; t++) recall[t] = (double)cnt[(size_t)t] / (double)denom;  // numpy int/int
+  return PSB_OK;
+}
+
 }  // extern "C"

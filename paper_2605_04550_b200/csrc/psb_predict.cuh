@@ -150,4 +150,32 @@ __global__ void k_region(const double* __restrict__ prob, int ny, int nx, double
   region[g] = v;
 }
 
+// calibrate_threshold's tau loop (pipeline.py:258-259) in one pass: dilate(prob >= tau, k) at a
+// pixel is (max of prob over the clipped k x k window) >= tau, so every tau is decided from one
+// window maximum. counts[t] += #{truth pixels with wmax >= taus[t]} (warp ballots, then one
+// shared-memory add per warp and one global add per block and tau).
+__global__ void k_recall(const double* __restrict__ prob, const uint8_t* __restrict__ truth, int ny, int nx, int k,
+                         const double* __restrict__ taus, int n_tau, unsigned long long* counts) {
+  extern __shared__ unsigned int cnt_s[];
+  for (int t = threadIdx.x; t < n_tau; t += blockDim.x) cnt_s[t] = 0;
+  __syncthreads();
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool on = false;
+  double m = -INFINITY;
+  if (g < (int64_t)ny * nx && truth[g]) {
+    on = true;
+    const int i = (int)(g / nx), j = (int)(g % nx), h = k / 2;
+    for (int ii = max(0, i - h); ii <= min(ny - 1, i + h); ii++)
+      for (int jj = max(0, j - h); jj <= min(nx - 1, j + h); jj++) m = fmax(m, prob[(int64_t)ii * nx + jj]);
+  }
+  const int lane = threadIdx.x & 31;
+  for (int t = 0; t < n_tau; t++) {
+    const unsigned b = __ballot_sync(0xffffffffu, on && m >= taus[t]);
+    if (lane == 0 && b) atomicAdd(&cnt_s[t], (unsigned)__popc(b));
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tau; t += blockDim.x)
+    if (cnt_s[t]) atomicAdd(&counts[t], (unsigned long long)cnt_s[t]);
+}
+
 }  // namespace psb

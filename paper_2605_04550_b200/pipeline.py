@@ -8,6 +8,8 @@ Mirrors, with the same names, arguments and results:
                                                  the host with numpy, fine points on K2)
   predicted_region       pipeline.py:227-231  -> K2 region kernel (>= tau, 5x5 dilation)
   hybrid_pseudospectrum  pipeline.py:273-297  -> K2 + restricted σ sweep on K1
+  calibrate_threshold    pipeline.py:241-270  -> full σ maps on K1, dense K2 maps, and the
+                                                 90-threshold recall loop in one K2 kernel
 and the host inputs they need: global_features (features.py:63-117, O(n^3) per matrix, host
 LAPACK as in the reference — SURVEY.md §8(f) row 1) and the model bundle format
 (network.py:35-52 PARAM_SHAPES, network.py:430-479 JSON document).
@@ -28,6 +30,7 @@ from .core import ComplexGrid, ModelFormatError, ParameterError, SigmaField
 
 TRUTH_DILATION = 3
 PRED_DILATION = 5
+CAL_TAUS = np.round(np.arange(0.05, 0.95, 0.01), 2)  # pipeline.py:25
 COORD_DIM, FEATURE_DIM = 26, 33
 PARAM_SHAPES = {
     "w_c1": (64, COORD_DIM), "b_c1": (64,), "w_c2": (64, 64), "b_c2": (64,),
@@ -279,6 +282,59 @@ def predicted_region(prob_field: np.ndarray, tau: float) -> np.ndarray:
     if rc != _lib.PSB_OK:
         raise RuntimeError(h.error())
     return region.astype(bool)
+
+
+def recall_sweep(prob_field: np.ndarray, truth_dil: np.ndarray, taus=CAL_TAUS,
+                 k: int = PRED_DILATION) -> np.ndarray:
+    """[_recall(dilate(prob >= t, k), truth_dil) for t in taus] (pipeline.py:234-238,258-259) in
+    one K2 kernel: the dilated mask at a pixel is (window max of prob) >= t."""
+    prob = np.ascontiguousarray(np.asarray(prob_field, dtype=float))
+    truth = np.ascontiguousarray(np.asarray(truth_dil, dtype=bool), dtype=np.uint8)
+    if prob.shape != truth.shape or prob.ndim != 2:
+        raise ParameterError(f"prob {prob.shape} and truth {truth.shape} must be equal 2-D shapes")
+    taus = np.ascontiguousarray(np.asarray(taus, dtype=float).ravel())
+    out = np.empty(taus.size)
+    ny, nx = prob.shape
+    h = _lib.handle()
+    with h.lock:
+        rc = h.lib.psb_recall_sweep(h.h, _lib._ptr(prob), _lib._ptr(truth), ny, nx, int(k), _lib._ptr(taus),
+                                    taus.size, _lib._ptr(out))
+    if rc != _lib.PSB_OK:
+        raise RuntimeError(h.error())
+    return out
+
+
+@dataclass
+class CalibrationReport:
+    taus: np.ndarray
+    median_recall: np.ndarray
+    p10_recall: np.ndarray
+    tau_star: float | None
+    passed: bool
+    recalls: np.ndarray = field(repr=False, default=None)  # (n_matrices, n_taus)
+
+
+def calibrate_threshold(bundle: ModelBundle, val_corpus, grid: ComplexGrid, eps: float,
+                        workers: int = 1) -> CalibrationReport:
+    """Smallest tau with median validation recall >= 0.90 and 10th-percentile recall >= 0.75
+    (pipeline.py:241-270). Per matrix: the exact σ map (K1), the dense probability map (K2) and
+    all 90 recalls (one K2 kernel). `workers` is accepted for signature compatibility."""
+    if not val_corpus:
+        raise ParameterError("validation corpus is empty")
+    recalls = np.empty((len(val_corpus), CAL_TAUS.size))
+    for row, entry in enumerate(val_corpus):
+        fld = core.full_pseudospectrum(entry.matrix, grid, label=f"matrix {entry.index}")
+        truth_dil = core.dilate(core.sensitive_zone(fld, eps), TRUTH_DILATION)
+        pmap = predict_map(bundle, entry.matrix, grid, probe_seed=entry.probe_seed)
+        recalls[row] = recall_sweep(pmap, truth_dil, CAL_TAUS, PRED_DILATION)
+    med = np.median(recalls, axis=0)
+    p10 = np.percentile(recalls, 10, axis=0)
+    passing = (med >= 0.90) & (p10 >= 0.75)
+    if passing.any():
+        best = int(np.argmax(passing))
+        return CalibrationReport(CAL_TAUS.copy(), med, p10, tau_star=float(CAL_TAUS[best]), passed=True,
+                                 recalls=recalls)
+    return CalibrationReport(CAL_TAUS.copy(), med, p10, tau_star=None, passed=False, recalls=recalls)
 
 
 @dataclass

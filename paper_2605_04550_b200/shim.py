@@ -3,7 +3,8 @@
 The reference has no plugin registry or FFI: its σ callers look `smin_many`,
 `full_pseudospectrum` and `restricted_field` up as module globals (core.py:187,207;
 pipeline.py:17-18; cli.py:22), and the predictor through `pipeline._predict_points`
-(pipeline.py:179,200,222). `install()` rebinds exactly those names (the substitution-point
+(pipeline.py:179,200,222); the field/mask writers as `io.write_*_csv` (cli.py:149-151).
+`install()` rebinds exactly those names (the substitution-point
 precedent is the reference's own tests, tests/test_pipeline.py:188 monkeypatching
 `pipeline.predict_map`), so every caller — cmd_compute, build_dataset, calibrate_threshold,
 hybrid_pseudospectrum, benchmark — runs on the GPU unchanged. Results come back as the
@@ -22,7 +23,7 @@ import functools
 
 import numpy as np
 
-from . import core, pipeline
+from . import core, io, pipeline
 
 _saved: list[tuple[object, str, object]] = []
 
@@ -55,6 +56,7 @@ def install(ps=None, predictor: bool = True):
     rcore = importlib.import_module(ps.__name__ + ".core")
     rpipe = importlib.import_module(ps.__name__ + ".pipeline")
     rcli = importlib.import_module(ps.__name__ + ".cli")
+    rio = importlib.import_module(ps.__name__ + ".io")
     tr = _translate(rcore)
 
     def _real(A):
@@ -88,6 +90,8 @@ def install(ps=None, predictor: bool = True):
         _patch(mod, "full_pseudospectrum", full_pseudospectrum)
     for mod in (rcore, rpipe):
         _patch(mod, "restricted_field", restricted_field)
+    _patch(rio, "write_field_csv", tr(io.write_field_csv))
+    _patch(rio, "write_mask_csv", tr(io.write_mask_csv))
     if hasattr(ps, "smin_many"):
         for name, fn in (("smin_many", smin_many), ("smin_at", smin_at),
                          ("full_pseudospectrum", full_pseudospectrum), ("restricted_field", restricted_field)):
@@ -110,8 +114,33 @@ def install(ps=None, predictor: bool = True):
                 raise rcore.ParameterError(f"tau must lie in (0, 1), got {tau}")
             return pipeline.predicted_region(prob_field, tau)
 
+        @tr
+        def calibrate_threshold(bundle, val_corpus, grid, eps, workers=1):
+            # pipeline.py:241-270 with the 90-threshold recall loop (258-259) on one K2 kernel;
+            # the σ maps and probability maps go through the rebound functions above
+            if not val_corpus:
+                raise rcore.ParameterError("validation corpus is empty")
+            taus = rpipe.CAL_TAUS
+            recalls = np.empty((len(val_corpus), taus.size))
+            for row, entry in enumerate(val_corpus):
+                fld = rpipe.full_pseudospectrum(entry.matrix, grid, label=f"matrix {entry.index}",
+                                                workers=workers)
+                truth_dil = rpipe.dilate(rpipe.sensitive_zone(fld, eps), rpipe.TRUTH_DILATION)
+                pmap = rpipe.predict_map(bundle, entry.matrix, grid, probe_seed=entry.probe_seed)
+                recalls[row] = pipeline.recall_sweep(pmap, truth_dil, taus, rpipe.PRED_DILATION)
+            med = np.median(recalls, axis=0)
+            p10 = np.percentile(recalls, 10, axis=0)
+            passing = (med >= 0.90) & (p10 >= 0.75)
+            if passing.any():
+                best = int(np.argmax(passing))
+                return rpipe.CalibrationReport(taus.copy(), med, p10, tau_star=float(taus[best]), passed=True,
+                                               recalls=recalls)
+            return rpipe.CalibrationReport(taus.copy(), med, p10, tau_star=None, passed=False, recalls=recalls)
+
         _patch(rpipe, "_predict_points", _predict_points)
         _patch(rpipe, "predicted_region", predicted_region)
+        _patch(rpipe, "calibrate_threshold", calibrate_threshold)
+        _patch(rcli, "calibrate_threshold", calibrate_threshold)
     return ps
 
 

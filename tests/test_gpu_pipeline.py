@@ -69,3 +69,53 @@ def test_region_kernel_matches_host_dilation(gpu):
     prob = rng.uniform(size=(37, 53)) ** 6
     for tau in (0.3, 0.7, 0.95):
         assert np.array_equal(pipeline.predicted_region(prob, tau), core.dilate(prob >= tau, 5))
+
+
+def _recall_loop(prob, truth, taus, k):
+    """The reference's tau loop, restated (pipeline.py:234-238,258-259; dilate = core.py:224-231)."""
+    from scipy.ndimage import binary_dilation
+    out = []
+    den = truth.sum()
+    for t in taus:
+        pred = binary_dilation(prob >= t, structure=np.ones((k, k), bool))
+        out.append(1.0 if den == 0 else float((pred & truth).sum() / den))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("shape,k", [((48, 48), 5), ((37, 91), 5), ((5, 3), 3), ((200, 200), 5)])
+def test_recall_sweep_matches_tau_loop(gpu, shape, k):
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1])
+    prob = rng.random(shape) ** 3
+    prob[rng.random(shape) < 0.1] = pipeline.CAL_TAUS[rng.integers(0, 90, 1)[0]]  # ties with a tau
+    truth = rng.random(shape) < 0.2
+    got = pipeline.recall_sweep(prob, truth, pipeline.CAL_TAUS, k)
+    assert np.array_equal(got, _recall_loop(prob, truth, pipeline.CAL_TAUS, k))
+    assert np.array_equal(pipeline.recall_sweep(prob, np.zeros(shape, bool)), np.ones(90))
+
+
+def test_calibrate_threshold_matches_reference(gpu, gold, bundle, refpkg_any):
+    """calibrate_threshold on 4 Grcar-family validation matrices vs the reference's own report,
+    run live on this host (exact), and vs the fixture made in the build container. The fixture
+    pins the outcome only loosely: the reference's predictor features come from host LAPACK
+    (eig / svd of a non-normal matrix), whose bits differ between CPU kernels, so a few
+    (matrix, tau) recalls differ between machines for the reference itself."""
+    from types import SimpleNamespace
+
+    from threadpoolctl import threadpool_limits
+    ps = refpkg_any
+    z = gold("calib_grcar.npz")
+    corpus = [SimpleNamespace(matrix=z[f"matrix_{i}"], index=int(z["indices"][i]),
+                              probe_seed=int(z["probe_seeds"][i])) for i in range(len(z["indices"]))]
+    grid = configs.make_grid(-1, 3, -3.5, 3.5, 48, 48)
+    rep = pipeline.calibrate_threshold(bundle, corpus, grid, 0.01)
+    mz = np.load(GOLD / "model_grcar.npz")
+    rb = ps.ModelBundle(params=ps.ModelParams(**{k: mz[k] for k in ps.network.PARAM_SHAPES}),
+                        feature_mean=mz["feature_mean"], feature_std=mz["feature_std"],
+                        tau_star=float(mz["tau_star"]))
+    rgrid = ps.make_grid(-1, 3, -3.5, 3.5, 48, 48)
+    with threadpool_limits(1):
+        want = ps.pipeline.calibrate_threshold(rb, corpus, rgrid, 0.01)
+    assert np.array_equal(rep.recalls, want.recalls)
+    assert rep.passed == want.passed and rep.tau_star == want.tau_star
+    assert rep.passed == bool(z["passed"]) and rep.tau_star == float(z["tau_star"])
+    assert np.max(np.abs(rep.recalls - z["recalls"])) <= 0.01

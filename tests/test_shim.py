@@ -67,3 +67,37 @@ def test_reference_pipeline_runs_on_gpu(gpu, refpkg_any):
         assert np.array_equal(res.field.values[res.region], full.values[res.region])
     finally:
         shim.uninstall()
+
+
+@pytest.mark.gpu
+def test_reference_calibrate_and_writers_run_on_gpu(gpu, refpkg_any, tmp_path):
+    """The reference's calibrate_threshold (recall loop on the K2 kernel) and CSV writers (native)
+    through the shim give the reference's own report and bytes."""
+    from threadpoolctl import threadpool_limits
+
+    import importlib
+
+    from paper_2605_04550_b200 import shim
+    ps = refpkg_any
+    importlib.import_module(ps.__name__ + ".io")
+    corpus = ps.generate_corpus(ps.GenSpec(n=24, seed=12), 2)
+    grid = ps.make_grid(-4, 4, -4, 4, 30, 30)
+    rng = np.random.default_rng(1)
+    params = ps.ModelParams(**{k: rng.standard_normal(s) * 0.1 for k, s in ps.network.PARAM_SHAPES.items()})
+    bundle = ps.ModelBundle(params=params, feature_mean=np.zeros(33), feature_std=np.ones(33), tau_star=0.3)
+    with threadpool_limits(1):
+        want = ps.pipeline.calibrate_threshold(bundle, corpus, grid, eps=0.05)
+        fld = ps.core.full_pseudospectrum(corpus[0].matrix, grid)
+        ps.io.write_field_csv(tmp_path / "ref.csv", fld)
+        ps.io.write_mask_csv(tmp_path / "refm.csv", fld.values <= 0.05, grid)
+    shim.install(ps)
+    try:
+        got = ps.pipeline.calibrate_threshold(bundle, corpus, grid, eps=0.05)
+        assert isinstance(got, ps.pipeline.CalibrationReport)
+        assert np.array_equal(got.recalls, want.recalls) and got.tau_star == want.tau_star
+        ps.io.write_field_csv(tmp_path / "ours.csv", fld)
+        ps.io.write_mask_csv(tmp_path / "oursm.csv", fld.values <= 0.05, grid)
+        assert (tmp_path / "ours.csv").read_bytes() == (tmp_path / "ref.csv").read_bytes()
+        assert (tmp_path / "oursm.csv").read_bytes() == (tmp_path / "refm.csv").read_bytes()
+    finally:
+        shim.uninstall()
