@@ -101,3 +101,24 @@ def test_reference_calibrate_and_writers_run_on_gpu(gpu, refpkg_any, tmp_path):
         assert (tmp_path / "oursm.csv").read_bytes() == (tmp_path / "refm.csv").read_bytes()
     finally:
         shim.uninstall()
+
+
+@pytest.mark.gpu
+def test_reference_build_dataset_labels_on_gpu(gpu, refpkg_any):
+    """the reference's build_dataset (its largest σ consumer) through the shim
+    gives the same balanced samples, features and labels as its own zgesdd path."""
+    from threadpoolctl import threadpool_limits
+
+    from paper_2605_04550_b200 import shim
+    ps = refpkg_any
+    corpus = ps.generate_corpus(ps.GenSpec(n=32, seed=21), 4)
+    grid = ps.make_grid(-4, 4, -4, 4, 36, 36)
+    with threadpool_limits(1):
+        want = ps.pipeline.build_dataset(corpus, grid, eps=0.05, seed=5)
+    shim.install(ps)
+    try:
+        got = ps.pipeline.build_dataset(corpus, grid, eps=0.05, seed=5)
+    finally:
+        shim.uninstall()
+    for name in ("xy", "features", "labels", "matrix_ids"):
+        assert np.array_equal(getattr(got, name), getattr(want, name)), name
