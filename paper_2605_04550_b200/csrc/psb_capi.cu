@@ -57,6 +57,7 @@ struct psb_handle {
   //   Lanczos warps, PSB_PROF=1 per-phase clock64 counters of the Lanczos kernel (stderr)
   bool k_secant = true, k_toeplitz = true, k_prof = false;
   long long k_lwarps = 0;
+  int k_btpb = 128;
   bool have_matrix = false;
   DevBuf Ab, AHA, v1;
   // per call
@@ -121,6 +122,7 @@ int psb_create(int device, psb_handle** out) {
   h->k_secant = getenv("PSB_NOSEC") == nullptr;
   h->k_toeplitz = getenv("PSB_NOTZ") == nullptr;
   h->k_prof = getenv("PSB_PROF") != nullptr;
+  h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 128;
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
@@ -376,16 +378,25 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   }
   // ---- engine B (bisection) on the caller's stream, sharing the SMs with engine L
   if (nB > 0) {
-    int occShare = occB;
-    if (nA > 0 && occB > 1) occShare = occB - 1;  // leave room for one engine-L block per SM
+    // Engine B fills what engine L leaves of each SM's register file (L: one 4-warp block per SM).
+    const int tpbB = h->k_btpb;
     int occM = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, kp.bm, 128, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, kp.bm, tpbB, 0));
     occM = std::max(occM, 1);
-    occShare = (nA > 0 && occM > 1) ? occM - 1 : occM;
-    gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, (nB * kp.g + 127) / 128));
+    int occShare = occM;
+    if (nA > 0) {
+      cudaFuncAttributes fb, fl;
+      CK(cudaFuncGetAttributes(&fb, kp.bm));
+      CK(cudaFuncGetAttributes(&fl, kp.l));
+      auto warp_regs = [](int r) { return (r * 32 + 255) / 256 * 256; };
+      const int regsL = warp_regs(fl.numRegs) * (int)(gridL > 0 ? kLWarpsPerBlock : 0);
+      const int regsB = warp_regs(fb.numRegs) * (tpbB / 32);
+      occShare = std::max(1, std::min(occM, (65536 - regsL) / regsB));
+    }
+    gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, (nB * kp.g + tpbB - 1) / tpbB));
     ba.mode = 1;
     ba.max_tests = 200;
-    kp.bm<<<(unsigned)gridB, 128, 0, st>>>(ba);
+    kp.bm<<<(unsigned)gridB, tpbB, 0, st>>>(ba);
     CK(cudaGetLastError());
   } else {
     gridB = 0;

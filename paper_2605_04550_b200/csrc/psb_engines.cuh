@@ -58,6 +58,11 @@ __device__ __forceinline__ void cp16(void* s, const void* g) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g) : "memory");
 }
+// zero-filling variant: copies `bytes` (0 or 16) and fills the rest of the 16 with zeros
+__device__ __forceinline__ void cp16z(void* s, const void* g, unsigned bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp4(void* s, const void* g) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g) : "memory");
@@ -84,51 +89,50 @@ __device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV 
                         const double2* __restrict__ v1, int k, double c1, double c2) {
   typedef Ring<KL, KU, D> RG;
   constexpr int W = RG::W, NU = RG::NU;
-  auto issue = [&](int j) {
-    if (j < n) {
-      const int sl = j % D;
+  // Branch-free in k (lanes of a warp sit at different k): X is v1 (k == 1) or T, and the RA / RB
+  // slots are zero-filled where the recurrence does not use them, so r = X - c1 RA - c2 RB with
+  // c1 = c2 = 0 at k == 1 and c2 = 0 at k == 2 reproduces the three cases bit for bit.
+  const double2* xsrc = (k == 1) ? v1 + R.lane : T.p;  // start vector: lane-replicated copy
+  const unsigned za = (k >= 2) ? 16u : 0u, zb = (k >= 3) ? 16u : 0u;
+  auto issue = [&](int j) {  // caller guarantees j < n
+    const int sl = j % D;
 #pragma unroll
-      for (int f = 0; f < NU; f++) cp16(R.at(sl, f), FU.p + ((int64_t)j * NU + f) * 32);
-      if (k >= 2) {
-        cp16(R.at(sl, NU), T.p + (int64_t)j * 32);
-        cp16(R.at(sl, NU + 1), RA.p + (int64_t)j * 32);
-        if (k >= 3) cp16(R.at(sl, NU + 2), RB.p + (int64_t)j * 32);
-      } else {
-        cp16(R.at(sl, NU), v1 + (int64_t)j * 32 + R.lane);  // start vector, lane-replicated copy
-      }
-    }
+    for (int f = 0; f < NU; f++) cp16(R.at(sl, f), FU.p + ((int64_t)j * NU + f) * 32);
+    cp16(R.at(sl, NU), xsrc + (int64_t)j * 32);
+    cp16z(R.at(sl, NU + 1), RA.p + (int64_t)j * 32, za);
+    cp16z(R.at(sl, NU + 2), RB.p + (int64_t)j * 32, zb);
     cp_commit();
   };
   double2 acc[W + 1];
 #pragma unroll
   for (int d = 0; d <= W; d++) acc[d] = czero();
   double bsq = 0.0;
-#pragma unroll
-  for (int q = 0; q < D - 1; q++) issue(q);
-#pragma unroll 2
-  for (int j = 0; j < n; j++) {
-    issue(j + D - 1);
-    cp_wait<D - 1>();
+  auto body = [&](int j) {
     const int sl = j % D;
-    double2 r;
-    if (k == 1) {
-      r = *R.at(sl, NU);
-      RA.put(j, r);
-    } else {
-      const double2 ra = *R.at(sl, NU + 1);
-      r = cfms_r(*R.at(sl, NU), c1, ra);
-      if (k >= 3) r = cfms_r(r, c2, *R.at(sl, NU + 2));
-      RB.put(j, ra);
-      RA.put(j, r);
-      bsq += cnorm2(r);
-    }
+    const double2 ra = *R.at(sl, NU + 1);
+    const double2 r = cfms_r(cfms_r(*R.at(sl, NU), c1, ra), c2, *R.at(sl, NU + 2));
+    RB.put(j, ra);
+    RA.put(j, r);
+    bsq += cnorm2(r);  // used for k >= 2 only
     const double2 tp = cadd(r, acc[0]);
     T.put(j, cmul(tp, cconj(*R.at(sl, W))));
 #pragma unroll
     for (int d = 1; d <= W; d++) acc[d - 1] = cfms_cj(acc[d], *R.at(sl, d - 1), tp);
     acc[W] = czero();
+  };
+  // prologue D-1 rows; steady state issues row j+D-1 unconditionally; the last D-1 rows drain
+#pragma unroll
+  for (int q = 0; q < D - 1; q++)
+    if (q < n) issue(q);
+  int j = 0;
+#pragma unroll 2
+  for (; j < n - (D - 1); j++) {
+    issue(j + D - 1);
+    cp_wait<D - 1>();
+    body(j);
   }
   cp_wait<0>();
+  for (; j < n; j++) body(j);
   return bsq;
 }
 
@@ -137,28 +141,21 @@ template <int KL, int KU, int D>
 __device__ double pl_s2(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T) {
   typedef Ring<KL, KU, D> RG;
   constexpr int NL = RG::NL;
-  auto issue = [&](int q) {
+  auto issue = [&](int q) {  // caller guarantees q < n
     const int j = n - 1 - q;
-    if (j >= 0) {
-      const int sl = q % D;
+    const int sl = q % D;
 #pragma unroll
-      for (int f = 0; f < KL; f++) cp16(R.at(sl, f), FL.p + ((int64_t)j * NL + f) * 32);
-      cp16(R.at(sl, NL), T.p + (int64_t)j * 32);
-      cp4(R.pat(sl), piv.p + (int64_t)j * 32);
-    }
+    for (int f = 0; f < KL; f++) cp16(R.at(sl, f), FL.p + ((int64_t)j * NL + f) * 32);
+    cp16(R.at(sl, NL), T.p + (int64_t)j * 32);
+    cp4(R.pat(sl), piv.p + (int64_t)j * 32);
     cp_commit();
   };
   double2 yw[KL + 1];
 #pragma unroll
   for (int r = 0; r <= KL; r++) yw[r] = czero();
   double nrm = 0.0;
-#pragma unroll
-  for (int q = 0; q < D - 1; q++) issue(q);
-#pragma unroll 2
-  for (int q = 0; q < n; q++) {
+  auto body = [&](int q) {
     const int j = n - 1 - q;
-    issue(q + D - 1);
-    cp_wait<D - 1>();
     const int sl = q % D;
     const int out = j + 1 + KL;
     if (out < n) { T.put(out, yw[KL]); nrm += cnorm2(yw[KL]); }
@@ -172,8 +169,19 @@ __device__ double pl_s2(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T) {
 #pragma unroll
     for (int r = 1; r <= KL; r++)
       if (p == r) { const double2 t = yw[0]; yw[0] = yw[r]; yw[r] = t; }
+  };
+#pragma unroll
+  for (int q = 0; q < D - 1; q++)
+    if (q < n) issue(q);
+  int q = 0;
+#pragma unroll 2
+  for (; q < n - (D - 1); q++) {
+    issue(q + D - 1);
+    cp_wait<D - 1>();
+    body(q);
   }
   cp_wait<0>();
+  for (; q < n; q++) body(q);
 #pragma unroll
   for (int r = 0; r <= KL; r++)
     if (r < n) { T.put(r, yw[r]); nrm += cnorm2(yw[r]); }
@@ -185,25 +193,19 @@ template <int KL, int KU, int D>
 __device__ void pl_s3(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T, double scale) {
   typedef Ring<KL, KU, D> RG;
   constexpr int NL = RG::NL;
-  auto issue = [&](int j) {
-    if (j < n) {
-      const int sl = j % D;
+  auto issue = [&](int j) {  // caller guarantees j < n; T row j+1+KL exists except for the last KL+1
+    const int sl = j % D;
 #pragma unroll
-      for (int f = 0; f < KL; f++) cp16(R.at(sl, f), FL.p + ((int64_t)j * NL + f) * 32);
-      if (j + 1 + KL < n) cp16(R.at(sl, NL), T.p + (int64_t)(j + 1 + KL) * 32);
-      cp4(R.pat(sl), piv.p + (int64_t)j * 32);
-    }
+    for (int f = 0; f < KL; f++) cp16(R.at(sl, f), FL.p + ((int64_t)j * NL + f) * 32);
+    const bool t_in = j + 1 + KL < n;
+    cp16z(R.at(sl, NL), T.p + (int64_t)(t_in ? j + 1 + KL : j) * 32, t_in ? 16u : 0u);
+    cp4(R.pat(sl), piv.p + (int64_t)j * 32);
     cp_commit();
   };
   double2 bw[KL + 1];
 #pragma unroll
   for (int r = 0; r <= KL; r++) bw[r] = (r < n) ? cscale(T.get(r), scale) : czero();
-#pragma unroll
-  for (int q = 0; q < D - 1; q++) issue(q);
-#pragma unroll 2
-  for (int j = 0; j < n; j++) {
-    issue(j + D - 1);
-    cp_wait<D - 1>();
+  auto body = [&](int j) {
     const int sl = j % D;
     const int p = *R.pat(sl);
 #pragma unroll
@@ -214,9 +216,20 @@ __device__ void pl_s3(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T, dou
     T.put(j, bw[0]);
 #pragma unroll
     for (int r = 0; r < KL; r++) bw[r] = bw[r + 1];
-    bw[KL] = (j + 1 + KL < n) ? cscale(*R.at(sl, NL), scale) : czero();
+    bw[KL] = cscale(*R.at(sl, NL), scale);  // zero-filled past the end
+  };
+#pragma unroll
+  for (int q = 0; q < D - 1; q++)
+    if (q < n) issue(q);
+  int j = 0;
+#pragma unroll 2
+  for (; j < n - (D - 1); j++) {
+    issue(j + D - 1);
+    cp_wait<D - 1>();
+    body(j);
   }
   cp_wait<0>();
+  for (; j < n; j++) body(j);
 }
 
 // S4 (backward): x = U^{-1}(scale*T) in place; returns sum Re(conj(RA_j) x_j).
@@ -225,28 +238,21 @@ template <int KL, int KU, int D>
 __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, double scale, double* wn2) {
   typedef Ring<KL, KU, D> RG;
   constexpr int W = RG::W, NU = RG::NU;
-  auto issue = [&](int q) {
+  auto issue = [&](int q) {  // caller guarantees q < n
     const int j = n - 1 - q;
-    if (j >= 0) {
-      const int sl = q % D;
+    const int sl = q % D;
 #pragma unroll
-      for (int f = 0; f < NU; f++) cp16(R.at(sl, f), FU.p + ((int64_t)j * NU + f) * 32);
-      cp16(R.at(sl, NU), T.p + (int64_t)j * 32);
-      cp16(R.at(sl, NU + 1), RA.p + (int64_t)j * 32);
-    }
+    for (int f = 0; f < NU; f++) cp16(R.at(sl, f), FU.p + ((int64_t)j * NU + f) * 32);
+    cp16(R.at(sl, NU), T.p + (int64_t)j * 32);
+    cp16(R.at(sl, NU + 1), RA.p + (int64_t)j * 32);
     cp_commit();
   };
   double2 xw[W + 1];
 #pragma unroll
   for (int c = 0; c <= W; c++) xw[c] = czero();
   double acc = 0.0, nn = 0.0;
-#pragma unroll
-  for (int q = 0; q < D - 1; q++) issue(q);
-#pragma unroll 2
-  for (int q = 0; q < n; q++) {
+  auto body = [&](int q) {
     const int j = n - 1 - q;
-    issue(q + D - 1);
-    cp_wait<D - 1>();
     const int sl = q % D;
     double2 x = cmul(cscale(*R.at(sl, NU), scale), *R.at(sl, W));
 #pragma unroll
@@ -257,8 +263,19 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
 #pragma unroll
     for (int c = W; c >= 2; c--) xw[c] = xw[c - 1];
     xw[1] = x;
+  };
+#pragma unroll
+  for (int q = 0; q < D - 1; q++)
+    if (q < n) issue(q);
+  int q = 0;
+#pragma unroll 2
+  for (; q < n - (D - 1); q++) {
+    issue(q + D - 1);
+    cp_wait<D - 1>();
+    body(q);
   }
   cp_wait<0>();
+  for (; q < n; q++) body(q);
   *wn2 = nn;
   return acc;
 }
