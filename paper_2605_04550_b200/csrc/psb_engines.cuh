@@ -94,8 +94,7 @@ __device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV 
   // c1 = c2 = 0 at k == 1 and c2 = 0 at k == 2 reproduces the three cases bit for bit.
   const double2* xsrc = (k == 1) ? v1 + R.lane : T.p;  // start vector: lane-replicated copy
   const unsigned za = (k >= 2) ? 16u : 0u, zb = (k >= 3) ? 16u : 0u;
-  auto issue = [&](int j) {  // caller guarantees j < n
-    const int sl = j % D;
+  auto issue = [&](int j, int sl) {  // caller guarantees j < n
 #pragma unroll
     for (int f = 0; f < NU; f++) cp16(R.at(sl, f), FU.p + ((int64_t)j * NU + f) * 32);
     cp16(R.at(sl, NU), xsrc + (int64_t)j * 32);
@@ -107,8 +106,7 @@ __device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV 
 #pragma unroll
   for (int d = 0; d <= W; d++) acc[d] = czero();
   double bsq = 0.0;
-  auto body = [&](int j) {
-    const int sl = j % D;
+  auto body = [&](int j, int sl) {
     const double2 ra = *R.at(sl, NU + 1);
     const double2 r = cfms_r(cfms_r(*R.at(sl, NU), c1, ra), c2, *R.at(sl, NU + 2));
     RB.put(j, ra);
@@ -123,16 +121,24 @@ __device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV 
   // prologue D-1 rows; steady state issues row j+D-1 unconditionally; the last D-1 rows drain
 #pragma unroll
   for (int q = 0; q < D - 1; q++)
-    if (q < n) issue(q);
+    if (q < n) issue(q, q);
+  // steady state in blocks of D rows, so every ring slot index is a compile-time constant
   int j = 0;
-#pragma unroll 2
+  for (; j + D <= n - (D - 1); j += D) {
+#pragma unroll
+    for (int u = 0; u < D; u++) {
+      issue(j + u + D - 1, (u + D - 1) % D);
+      cp_wait<D - 1>();
+      body(j + u, u);
+    }
+  }
   for (; j < n - (D - 1); j++) {
-    issue(j + D - 1);
+    issue(j + D - 1, (j + D - 1) % D);
     cp_wait<D - 1>();
-    body(j);
+    body(j, j % D);
   }
   cp_wait<0>();
-  for (; j < n; j++) body(j);
+  for (; j < n; j++) body(j, j % D);
   return bsq;
 }
 
@@ -141,9 +147,8 @@ template <int KL, int KU, int D>
 __device__ double pl_s2(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T) {
   typedef Ring<KL, KU, D> RG;
   constexpr int NL = RG::NL;
-  auto issue = [&](int q) {  // caller guarantees q < n
+  auto issue = [&](int q, int sl) {  // caller guarantees q < n
     const int j = n - 1 - q;
-    const int sl = q % D;
 #pragma unroll
     for (int f = 0; f < KL; f++) cp16(R.at(sl, f), FL.p + ((int64_t)j * NL + f) * 32);
     cp16(R.at(sl, NL), T.p + (int64_t)j * 32);
@@ -154,9 +159,8 @@ __device__ double pl_s2(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T) {
 #pragma unroll
   for (int r = 0; r <= KL; r++) yw[r] = czero();
   double nrm = 0.0;
-  auto body = [&](int q) {
+  auto body = [&](int q, int sl) {
     const int j = n - 1 - q;
-    const int sl = q % D;
     const int out = j + 1 + KL;
     if (out < n) { T.put(out, yw[KL]); nrm += cnorm2(yw[KL]); }
 #pragma unroll
@@ -172,16 +176,24 @@ __device__ double pl_s2(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T) {
   };
 #pragma unroll
   for (int q = 0; q < D - 1; q++)
-    if (q < n) issue(q);
+    if (q < n) issue(q, q);
+  // steady state in blocks of D rows, so every ring slot index is a compile-time constant
   int q = 0;
-#pragma unroll 2
+  for (; q + D <= n - (D - 1); q += D) {
+#pragma unroll
+    for (int u = 0; u < D; u++) {
+      issue(q + u + D - 1, (u + D - 1) % D);
+      cp_wait<D - 1>();
+      body(q + u, u);
+    }
+  }
   for (; q < n - (D - 1); q++) {
-    issue(q + D - 1);
+    issue(q + D - 1, (q + D - 1) % D);
     cp_wait<D - 1>();
-    body(q);
+    body(q, q % D);
   }
   cp_wait<0>();
-  for (; q < n; q++) body(q);
+  for (; q < n; q++) body(q, q % D);
 #pragma unroll
   for (int r = 0; r <= KL; r++)
     if (r < n) { T.put(r, yw[r]); nrm += cnorm2(yw[r]); }
@@ -193,8 +205,7 @@ template <int KL, int KU, int D>
 __device__ void pl_s3(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T, double scale) {
   typedef Ring<KL, KU, D> RG;
   constexpr int NL = RG::NL;
-  auto issue = [&](int j) {  // caller guarantees j < n; T row j+1+KL exists except for the last KL+1
-    const int sl = j % D;
+  auto issue = [&](int j, int sl) {  // caller guarantees j < n; T row j+1+KL exists except for the last KL+1
 #pragma unroll
     for (int f = 0; f < KL; f++) cp16(R.at(sl, f), FL.p + ((int64_t)j * NL + f) * 32);
     const bool t_in = j + 1 + KL < n;
@@ -205,8 +216,7 @@ __device__ void pl_s3(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T, dou
   double2 bw[KL + 1];
 #pragma unroll
   for (int r = 0; r <= KL; r++) bw[r] = (r < n) ? cscale(T.get(r), scale) : czero();
-  auto body = [&](int j) {
-    const int sl = j % D;
+  auto body = [&](int j, int sl) {
     const int p = *R.pat(sl);
 #pragma unroll
     for (int r = 1; r <= KL; r++)
@@ -220,16 +230,24 @@ __device__ void pl_s3(int n, const Ring<KL, KU, D>& R, LV FL, LVb piv, LV T, dou
   };
 #pragma unroll
   for (int q = 0; q < D - 1; q++)
-    if (q < n) issue(q);
+    if (q < n) issue(q, q);
+  // steady state in blocks of D rows, so every ring slot index is a compile-time constant
   int j = 0;
-#pragma unroll 2
+  for (; j + D <= n - (D - 1); j += D) {
+#pragma unroll
+    for (int u = 0; u < D; u++) {
+      issue(j + u + D - 1, (u + D - 1) % D);
+      cp_wait<D - 1>();
+      body(j + u, u);
+    }
+  }
   for (; j < n - (D - 1); j++) {
-    issue(j + D - 1);
+    issue(j + D - 1, (j + D - 1) % D);
     cp_wait<D - 1>();
-    body(j);
+    body(j, j % D);
   }
   cp_wait<0>();
-  for (; j < n; j++) body(j);
+  for (; j < n; j++) body(j, j % D);
 }
 
 // S4 (backward): x = U^{-1}(scale*T) in place; returns sum Re(conj(RA_j) x_j).
@@ -238,9 +256,8 @@ template <int KL, int KU, int D>
 __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, double scale, double* wn2) {
   typedef Ring<KL, KU, D> RG;
   constexpr int W = RG::W, NU = RG::NU;
-  auto issue = [&](int q) {  // caller guarantees q < n
+  auto issue = [&](int q, int sl) {  // caller guarantees q < n
     const int j = n - 1 - q;
-    const int sl = q % D;
 #pragma unroll
     for (int f = 0; f < NU; f++) cp16(R.at(sl, f), FU.p + ((int64_t)j * NU + f) * 32);
     cp16(R.at(sl, NU), T.p + (int64_t)j * 32);
@@ -251,9 +268,8 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
 #pragma unroll
   for (int c = 0; c <= W; c++) xw[c] = czero();
   double acc = 0.0, nn = 0.0;
-  auto body = [&](int q) {
+  auto body = [&](int q, int sl) {
     const int j = n - 1 - q;
-    const int sl = q % D;
     double2 x = cmul(cscale(*R.at(sl, NU), scale), *R.at(sl, W));
 #pragma unroll
     for (int c = W; c >= 1; c--) x = cfms(x, *R.at(sl, c - 1), xw[c]);
@@ -266,16 +282,24 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
   };
 #pragma unroll
   for (int q = 0; q < D - 1; q++)
-    if (q < n) issue(q);
+    if (q < n) issue(q, q);
+  // steady state in blocks of D rows, so every ring slot index is a compile-time constant
   int q = 0;
-#pragma unroll 2
+  for (; q + D <= n - (D - 1); q += D) {
+#pragma unroll
+    for (int u = 0; u < D; u++) {
+      issue(q + u + D - 1, (u + D - 1) % D);
+      cp_wait<D - 1>();
+      body(q + u, u);
+    }
+  }
   for (; q < n - (D - 1); q++) {
-    issue(q + D - 1);
+    issue(q + D - 1, (q + D - 1) % D);
     cp_wait<D - 1>();
-    body(q);
+    body(q, q % D);
   }
   cp_wait<0>();
-  for (; q < n; q++) body(q);
+  for (; q < n; q++) body(q, q % D);
   *wn2 = nn;
   return acc;
 }
