@@ -320,7 +320,7 @@ def run_ours(args, rank, world, local_rank):
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(dom)
+            traffic = json.loads(tf.read_text()).get(args.config, {}).get(dom)
         except Exception:
             traffic = None
     roof = dict(kern[dom])
