@@ -84,6 +84,7 @@ struct Ring {
 
 // S1 (forward): r_k update and t = U^{-H} r_k, right-looking so row j's U' entries are consumed
 // at step j (the ring holds current/future rows only). Slot j: FU_j | T_j RA_j RB_j.
+// RA holds r_{k-1}, RB r_{k-2}; r_k is written over RB and the caller swaps the two roles.
 template <int KL, int KU, int D>
 __device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV RB,
                         const double2* __restrict__ v1, int k, double c1, double c2) {
@@ -107,10 +108,8 @@ __device__ double pl_s1(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, LV 
   for (int d = 0; d <= W; d++) acc[d] = czero();
   double bsq = 0.0;
   auto body = [&](int j, int sl) {
-    const double2 ra = *R.at(sl, NU + 1);
-    const double2 r = cfms_r(cfms_r(*R.at(sl, NU), c1, ra), c2, *R.at(sl, NU + 2));
-    RB.put(j, ra);
-    RA.put(j, r);
+    const double2 r = cfms_r(cfms_r(*R.at(sl, NU), c1, *R.at(sl, NU + 1)), c2, *R.at(sl, NU + 2));
+    RB.put(j, r);  // r_k overwrites r_{k-2} (row j already consumed); the caller swaps RA / RB
     bsq += cnorm2(r);  // used for k >= 2 only
     const double2 tp = cadd(r, acc[0]);
     T.put(j, cmul(tp, cconj(*R.at(sl, W))));
@@ -570,8 +569,9 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
   const LV FL{base + (int64_t)n * s.NU * 32 + lane, 32};
   const int64_t vo = (int64_t)n * (s.NU + s.NL) * 32;
   const LV T{base + vo + lane, 32};
-  const LV RA{base + vo + (int64_t)n * 32 + lane, 32};
-  const LV RB{base + vo + (int64_t)n * 64 + lane, 32};
+  const LV RA0{base + vo + (int64_t)n * 32 + lane, 32};
+  const LV RB0{base + vo + (int64_t)n * 64 + lane, 32};
+  bool rsw = false;  // static shapes rotate the two residual buffers (RA = newest) instead of copying
   double2* hist = base + vo + (int64_t)n * 96 + lane;
   const LVb piv{a.pivs + gw * a.piv_stride + lane, 32};
   typedef Ring<(KL > 0 ? KL : 1), KU, DPIPE> RG;
@@ -641,8 +641,11 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       const double c1 = (k >= 2) ? aprev / b1 : 0.0;
       const double c2 = (k >= 3) ? b1 / b2 : 0.0;
       double bsq;
-      if constexpr (DYN) bsq = sweep_s1<KL, KU, DYN>(s, FU, T, RA, RB, a.v1, k, c1, c2);
-      else bsq = pl_s1<KL, KU, DPIPE>(n, ring, FU, T, RA, RB, a.v1, k, c1, c2);
+      if constexpr (DYN) bsq = sweep_s1<KL, KU, DYN>(s, FU, T, RA0, RB0, a.v1, k, c1, c2);
+      else {
+        bsq = pl_s1<KL, KU, DPIPE>(n, ring, FU, T, rsw ? RB0 : RA0, rsw ? RA0 : RB0, a.v1, k, c1, c2);
+        rsw = !rsw;
+      }
       if (a.prof) { long long t = clock64(); if (__activemask() && lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[1], (unsigned long long)(t - tq1)); tq1 = t; }
       if (k >= 2) {
         const double beta = sqrt(bsq);  // beta_{k-1}
@@ -675,11 +678,11 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       double acc, wn2 = 0.0;
       if constexpr (DYN) {
         sweep_s3<KL, KU, DYN>(s, FL, piv, T, 1.0 / (nu * b1));
-        acc = sweep_s4<KL, KU, DYN>(s, FU, T, RA, 1.0 / nu, &wn2);
+        acc = sweep_s4<KL, KU, DYN>(s, FU, T, RA0, 1.0 / nu, &wn2);
       } else {
         pl_s3<KL, KU, DPIPE>(n, ring, FL, piv, T, 1.0 / (nu * b1));
         if (a.prof) { long long t = clock64(); if (lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[3], (unsigned long long)(t - tq1)); tq1 = t; }
-        acc = pl_s4<KL, KU, DPIPE>(n, ring, FU, T, RA, 1.0 / nu, &wn2);
+        acc = pl_s4<KL, KU, DPIPE>(n, ring, FU, T, rsw ? RB0 : RA0, 1.0 / nu, &wn2);
         if (a.prof) { long long t = clock64(); if (lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[4], (unsigned long long)(t - tq1)); tq1 = t; }
       }
       const double alpha = acc / b1;
