@@ -262,8 +262,8 @@ static double flops_it_row(int kl, int ku) {
 static double bytes_it_row(int kl, int ku) {
   const int W = kl + ku;
   // factors read twice per step (S1,S4: U' + rinv; S2,S3: L) + int32 pivots twice;
-  // vectors: S1 r3 w3, S2 r1 w1, S3 r1 w1, S4 r2 w1
-  return 16.0 * (2.0 * (W + 1) + 2.0 * kl) + 8.0 + 16.0 * (6 + 2 + 2 + 3);
+  // vectors (steady state, k >= 3): S1 r3 w2 (the residual buffers rotate), S2 r1 w1, S3 r1 w1, S4 r2 w1
+  return 16.0 * (2.0 * (W + 1) + 2.0 * kl) + 8.0 + 16.0 * (5 + 2 + 2 + 3);
 }
 
 // Core pipeline on device buffers. zs/outidx/out/iters/status are device pointers.
