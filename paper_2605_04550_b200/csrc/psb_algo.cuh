@@ -128,8 +128,16 @@ PSB_HD Shape make_shape(int n, int kl, int ku) {
 // Pivoted LU of M = zI - A in a sliding register window of (kl+1) rows x (W+1)
 // columns. Pivot rule: first max of |re|+|im| (LAPACK izamax/dcabs1 convention,
 // as zgbtrf). Returns false on an exactly zero pivot (M singular in floating point).
-template <int KLM, int KUM, bool DYN>
-PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z, LV FU, LV FL, LVb piv) {
+struct NoRowHook {
+  template <int N>
+  PSB_HD void operator()(int, const double2 (&)[N]) const {}
+};
+
+// `hook(j, u)` sees each finished U row (u[0..W-1] = U', u[W] = rinv) in forward order, so a
+// forward sweep that needs exactly these rows can run fused with the factorization.
+template <int KLM, int KUM, bool DYN, class RowHook = NoRowHook>
+PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z, LV FU, LV FL, LVb piv,
+                      RowHook hook = RowHook()) {
   constexpr int WM = KLM + KUM;
   const int n = s.n;
   const int kl = DYN ? s.kl : KLM;
@@ -180,10 +188,16 @@ PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z,
     if (d.x == 0.0 && d.y == 0.0) { ok = false; ri = czero(); }
     else ri = crcp_fast(d);
     const int64_t rb = (int64_t)j * NU;
+    double2 u[WM + 1];
 #pragma unroll
     for (int c = 1; c <= WM; c++)
-      if (c <= W) FU.put(rb + c - 1, cmul(win[0][c], ri));
+      if (c <= W) {
+        u[c - 1] = cmul(win[0][c], ri);
+        FU.put(rb + c - 1, u[c - 1]);
+      }
+    u[DYN ? WM : W] = ri;  // static shapes: u[W] = rinv (the hook is static-shape only)
     FU.put(rb + W, ri);
+    hook(j, u);
 #pragma unroll
     for (int r = 1; r <= KLM; r++) {
       if (r <= kl) {

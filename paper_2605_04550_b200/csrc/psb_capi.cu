@@ -359,6 +359,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     LanArgs la;
     la.s = s; la.Ab = h->Ab.as<double2>();
     la.v1 = dyn ? h->v1.as<double2>() : h->v1.as<double2>() + n;  // pipelined sweeps read the replicated copy
+    la.v1b = h->v1.as<double2>();
     la.zs = d_zs; la.outidx = d_outidx; la.listA = h->listA.as<int64_t>(); la.counters = cnt;
     la.out = d_out; la.iters = d_iters; la.status = d_status;
     la.scratch = h->scratch.as<double2>(); la.pivs = h->pivs.as<int>();

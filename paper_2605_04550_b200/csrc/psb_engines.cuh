@@ -36,6 +36,7 @@ struct LanArgs {
   Shape s;
   const double2* __restrict__ Ab;
   const double2* __restrict__ v1;
+  const double2* __restrict__ v1b;  // v1 once (n entries): warp-uniform loads in the fused LU + S1
   const double2* __restrict__ zs;
   const int64_t* __restrict__ outidx;
   const int64_t* __restrict__ listA;
@@ -572,6 +573,7 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
   const LV RA0{base + vo + (int64_t)n * 32 + lane, 32};
   const LV RB0{base + vo + (int64_t)n * 64 + lane, 32};
   bool rsw = false;  // static shapes rotate the two residual buffers (RA = newest) instead of copying
+  bool s1done = false;  // step 1's S1 already ran fused with the LU
   double2* hist = base + vo + (int64_t)n * 96 + lane;
   const LVb piv{a.pivs + gw * a.piv_stride + lane, 32};
   typedef Ring<(KL > 0 ? KL : 1), KU, DPIPE> RG;
@@ -622,11 +624,35 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
     }
     long long tq0 = clock64();
     if (phase == 1) {
-      const bool ok = lu_factor<KL, KU, DYN>(s, a.Ab, z, FU, FL, piv);
+      bool ok;
+      if constexpr (DYN) {
+        ok = lu_factor<KL, KU, DYN>(s, a.Ab, z, FU, FL, piv);
+      } else {
+        // LU fused with S1 of step 1 (t = U^{-H} v1): the same arithmetic as pl_s1 at k = 1
+        // (r = v1 exactly), on the U rows as the factorization produces them
+        constexpr int W = KL + KU;
+        const LV Tn = T, Rn = rsw ? RA0 : RB0;  // pl_s1 writes r into the current RB, then swaps
+        double2 acc[W + 1];
+#pragma unroll
+        for (int d = 0; d <= W; d++) acc[d] = czero();
+        const double2* __restrict__ v1b = a.v1b;
+        double2 vnext = v1b[0];  // one row ahead
+        ok = lu_factor<KL, KU, DYN>(s, a.Ab, z, FU, FL, piv, [&](int j, const double2 (&u)[W + 1]) {
+          const double2 r = vnext;
+          if (j + 1 < n) vnext = v1b[j + 1];
+          Rn.put(j, r);
+          const double2 tp = cadd(r, acc[0]);
+          Tn.put(j, cmul(tp, cconj(u[W])));
+#pragma unroll
+          for (int d = 1; d <= W; d++) acc[d - 1] = cfms_cj(acc[d], u[d - 1], tp);
+          acc[W] = czero();
+        });
+      }
       if (!ok) {
         finish(0.0, 0, 2);
       } else {
         phase = 2; k = 1; nu = 1.0; b1 = 1.0; b2 = 1.0; aprev = 0.0; theta = 0.0; s2 = 1.0; dth = 0.0;
+        if constexpr (!DYN) { s1done = true; rsw = !rsw; }
       }
     }
     long long tq1 = clock64();
@@ -636,7 +662,9 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       if (exhausted && __ballot_sync(FULL, phase != 0) == 0) break;
       continue;
     }
-    if (phase == 2) {
+    if (phase == 2 && s1done) {
+      s1done = false;
+    } else if (phase == 2) {
       // S1: r_k and U^{-H} r_k
       const double c1 = (k >= 2) ? aprev / b1 : 0.0;
       const double c2 = (k >= 3) ? b1 / b2 : 0.0;
