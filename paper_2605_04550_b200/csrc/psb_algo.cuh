@@ -162,6 +162,9 @@ PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z,
       win[r][c] = v;
     }
   }
+  double2 pre[WM + 1];
+#pragma unroll
+  for (int c = 0; c <= WM; c++) pre[c] = (c <= W && kl + 1 < n) ? Ab[(int64_t)c * n + kl + 1] : czero();
   for (int j = 0; j < n; j++) {
     // pivot among rows j..j+kl (rows past n are zero and never win a strict '>')
     int p = 0;
@@ -218,18 +221,17 @@ PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z,
         win[r][W < WM ? W : WM] = czero();
       }
     }
-    // new bottom row: matrix row i = j+1+kl, columns j+1 .. j+1+W (d = c - kl)
+    // new bottom row: matrix row i = j+1+kl, columns j+1 .. j+1+W (d = c - kl); its band
+    // entries were loaded one row earlier (pre), and row i+1's are loaded now
     const int i = j + 1 + kl;
 #pragma unroll
     for (int c = 0; c <= WM; c++) {
       if (c <= W) {
         double2 v = czero();
         int col = j + 1 + c;
-        if (i < n && col < n) {
-          double2 a = Ab[(int64_t)c * n + i];
-          v = cmk((c == kl ? z.x : 0.0) - a.x, (c == kl ? z.y : 0.0) - a.y);
-        }
+        if (i < n && col < n) v = cmk((c == kl ? z.x : 0.0) - pre[c].x, (c == kl ? z.y : 0.0) - pre[c].y);
         win[kl][c] = v;
+        pre[c] = (i + 1 < n) ? Ab[(int64_t)c * n + i + 1] : czero();
       }
     }
   }
