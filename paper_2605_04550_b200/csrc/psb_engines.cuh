@@ -430,53 +430,53 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       const bool tz = a.tz_j0 <= a.tz_j1;
 #pragma unroll
       for (int d = 0; d <= B; d++) gc[d] = tz ? g_entry<KL, KU>(a.n, a.tz_j0, d, a.Ab, a.AHA, zt, 0.0) : czero();
-      auto load_new = [&](int i) {
-        if (tz && i >= a.tz_j0 && i <= a.tz_j1) pdw_load_row_g<KL, KU, NP>(Wn, B, gc, zz);
-        else pdw_load_row<KL, KU, NP>(Wn, B, a.n, i, a.Ab, a.AHA, zt, zz);
-      };
 #pragma unroll
       for (int r = 0; r <= B; r++) pdw_load_row<KL, KU, NP>(Wn, r, a.n, r, a.Ab, a.AHA, zt, zz);
-      if constexpr (!SEC) {
-#pragma unroll 4
-        for (int j = 0; j < a.n; j++) {
-          pdw_step<KL, KU, NP, false>(Wn, pd, ld);
-          load_new(j + 1 + B);
-          if ((j & 31) == 31) {
+      // Rows run in three segments so no row carries a loader branch: step j loads matrix row
+      // j+1+B, which lies in the diagonal-constant interior [tz_j0, tz_j1] for j in [J0, J1).
+      // Inside a segment, 8-row blocks are straight-line code (the window shift is register
+      // renaming); log-det renormalisation and the all-failed vote sit between blocks.
+      int J0 = a.n, J1 = a.n;
+      if (tz) {
+        J0 = min(max(a.tz_j0 - 1 - B, 0), a.n);
+        J1 = min(max(a.tz_j1 - B, J0), a.n);
+      }
+      bool stop = false;
+      auto run = [&](int j0, int j1, auto&& loader) {
+        int j = j0;
+        for (; !stop && j + 8 <= j1; j += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+            loader(j + u + 1 + B);
+          }
+          if constexpr (SEC) {
+#pragma unroll
+            for (int q = 0; q < NP; q++) ld[q].norm();
+          }
+          if (((j - j0) & 31) == 24) {
             bool any = false;
 #pragma unroll
             for (int q = 0; q < NP; q++) any = any || pd[q];
-            if (!__any_sync(FULL, any && me)) break;  // every probe of every active lane failed
+            if (!__any_sync(FULL, any && me)) stop = true;  // every probe of every active lane failed
           }
         }
-      } else {
-      // 8-row blocks without branches inside (log-det renormalisation and the early-exit vote
-      // between blocks), then the remainder rows
-      const int nb = a.n & ~7;
-      int j = 0;
-      for (; j < nb; j += 8) {
+        if (!stop) {
+          for (; j < j1; j++) {
+            pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+            loader(j + 1 + B);
+          }
+          if constexpr (SEC) {
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
-          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
-          load_new(j + u + 1 + B);
+            for (int q = 0; q < NP; q++) ld[q].norm();
+          }
         }
-        if constexpr (SEC) {
-#pragma unroll
-          for (int q = 0; q < NP; q++) ld[q].norm();
-        }
-        if ((j & 31) == 24) {
-          bool any = false;
-#pragma unroll
-          for (int q = 0; q < NP; q++) any = any || pd[q];
-          if (!__any_sync(FULL, any && me)) break;  // every probe of every active lane failed
-        }
-      }
-      if (j >= nb) {
-        for (; j < a.n; j++) {
-          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
-          load_new(j + 1 + B);
-        }
-      }
-      }
+      };
+      auto load_gen = [&](int i) { pdw_load_row<KL, KU, NP>(Wn, B, a.n, i, a.Ab, a.AHA, zt, zz); };
+      auto load_tz = [&](int) { pdw_load_row_g<KL, KU, NP>(Wn, B, gc, zz); };
+      run(0, J0, load_gen);
+      run(J0, J1, load_tz);
+      run(J1, a.n, load_gen);
     }
     if (a.mode == 0) {
       // warp-aggregated appends keep a warp's consecutive (spatially adjacent) points together in
