@@ -442,7 +442,20 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         J1 = min(max(a.tz_j1 - B, J0), a.n);
       }
       bool stop = false;
-      auto run = [&](int j0, int j1, auto&& loader) {
+      auto vote = [&]() {
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < NP; q++) any = any || pd[q];
+        if (!__any_sync(FULL, any && me)) stop = true;  // every probe of every active lane failed
+      };
+      auto norm = [&]() {
+        if constexpr (SEC) {
+#pragma unroll
+          for (int q = 0; q < NP; q++) ld[q].norm();
+        }
+      };
+      // rows [j0, j1) in straight-line 8-row blocks, then the remainder
+      auto run8 = [&](int j0, int j1, auto&& loader) {
         int j = j0;
         for (; !stop && j + 8 <= j1; j += 8) {
 #pragma unroll
@@ -450,33 +463,32 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
             pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
             loader(j + u + 1 + B);
           }
-          if constexpr (SEC) {
-#pragma unroll
-            for (int q = 0; q < NP; q++) ld[q].norm();
-          }
-          if (((j - j0) & 31) == 24) {
-            bool any = false;
-#pragma unroll
-            for (int q = 0; q < NP; q++) any = any || pd[q];
-            if (!__any_sync(FULL, any && me)) stop = true;  // every probe of every active lane failed
-          }
+          norm();
+          if (((j - j0) & 31) == 24) vote();
         }
-        if (!stop) {
-          for (; j < j1; j++) {
-            pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
-            loader(j + 1 + B);
-          }
-          if constexpr (SEC) {
-#pragma unroll
-            for (int q = 0; q < NP; q++) ld[q].norm();
-          }
+        for (; !stop && j < j1; j++) {
+          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+          loader(j + 1 + B);
+          if (((j - j0) & 7) == 7) norm();
         }
+        norm();
       };
-      auto load_gen = [&](int i) { pdw_load_row<KL, KU, NP>(Wn, B, a.n, i, a.Ab, a.AHA, zt, zz); };
-      auto load_tz = [&](int) { pdw_load_row_g<KL, KU, NP>(Wn, B, gc, zz); };
-      run(0, J0, load_gen);
-      run(J0, J1, load_tz);
-      run(J1, a.n, load_gen);
+      // short edge segments: a plain row loop (keeps the unrolled code, and registers, to one body)
+      auto run1 = [&](int j0, int j1) {
+        for (int j = j0; j < j1; j++) {
+          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+          pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + 1 + B, a.Ab, a.AHA, zt, zz);
+          if (((j - j0) & 7) == 7) norm();
+        }
+        norm();
+      };
+      if (tz) {
+        run1(0, J0);
+        run8(J0, J1, [&](int) { pdw_load_row_g<KL, KU, NP>(Wn, B, gc, zz); });
+        if (!stop) run1(J1, a.n);
+      } else {
+        run8(0, a.n, [&](int i) { pdw_load_row<KL, KU, NP>(Wn, B, a.n, i, a.Ab, a.AHA, zt, zz); });
+      }
     }
     if (a.mode == 0) {
       // warp-aggregated appends keep a warp's consecutive (spatially adjacent) points together in
