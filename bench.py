@@ -294,7 +294,8 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * P / (float(te.item()) * 1e-3)
-    h2d = P * 16 + (P * 8 if world == 1 else 0)          # shifts (+ output index map on the grid path)
+    # grid path: the two axes (shifts are formed on the device); sharded path: this rank's shifts
+    h2d = (grid.nx + grid.ny) * 8 if world == 1 else P * 16
     d2h = (grid.size * 9) if world == 1 else P * 9       # sigma (f64) + status (i8)
 
     # ---- roofline of the dominant kernel

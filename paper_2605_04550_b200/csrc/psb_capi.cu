@@ -39,6 +39,25 @@ struct DevBuf {
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// Pinned host staging: copies between pageable caller buffers and the device go through it, so
+// every cudaMemcpyAsync is a direct DMA (a memcpy on each side of the call is far cheaper than
+// the driver's pageable staging).
+struct PinBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr; cap = 0;
+    size_t want = std::max<size_t>(bytes, 4096);
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocDefault);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() { if (p) cudaFreeHost(p); p = nullptr; cap = 0; }
+  template <class T> T* at(size_t byte_off) const { return reinterpret_cast<T*>((char*)p + byte_off); }
+};
+
 }  // namespace
 
 struct psb_handle {
@@ -63,6 +82,7 @@ struct psb_handle {
   // per call
   DevBuf zs, outidx, out, iters, status, listA, listB, counters, scratch, pivs, dynL, dynD;
   DevBuf xs, ys, prof;
+  PinBuf pin;
   // predictor
   DevBuf params, feat, eig, prob, region, idx;
   psb_stats stats{};
@@ -138,6 +158,7 @@ void psb_destroy(psb_handle* h) {
                     &h->counters, &h->scratch, &h->pivs, &h->dynL, &h->dynD, &h->xs, &h->ys, &h->params,
                     &h->feat, &h->eig, &h->prob, &h->region, &h->idx};
   for (DevBuf* b : bufs) b->release();
+  h->pin.release();
   for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
   if (h->stream) cudaStreamDestroy(h->stream);
   if (h->stream2) cudaStreamDestroy(h->stream2);
@@ -484,17 +505,22 @@ int psb_smin_points(psb_handle* h, const double* zs, int64_t P, const psb_opts* 
   CK(h->out.ensure(sizeof(double) * P));
   CK(h->iters.ensure(sizeof(int32_t) * P));
   CK(h->status.ensure(sizeof(int8_t) * P));
-  CK(cudaMemcpyAsync(h->zs.p, zs, sizeof(double2) * P, cudaMemcpyHostToDevice, st));
+  // pinned staging: [zs | sigma | iters | status]
+  const size_t oz = 0, os = oz + 16 * (size_t)P, oi = os + 8 * (size_t)P, ot = oi + 4 * (size_t)P;
+  CK(h->pin.ensure(ot + (size_t)P));
+  std::memcpy(h->pin.at<char>(oz), zs, 16 * (size_t)P);
+  CK(cudaMemcpyAsync(h->zs.p, h->pin.at<char>(oz), sizeof(double2) * P, cudaMemcpyHostToDevice, st));
   int rc = run_pipeline(h, h->zs.as<double2>(), nullptr, P, h->out.as<double>(), h->iters.as<int32_t>(),
                         h->status.as<int8_t>(), opts, st);
   if (rc != PSB_OK) return rc;
-  std::vector<int8_t> stat_local;
-  int8_t* stat_h = status;
-  if (!stat_h) { stat_local.resize(P); stat_h = stat_local.data(); }
-  CK(cudaMemcpyAsync(sigma, h->out.p, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
-  if (iters) CK(cudaMemcpyAsync(iters, h->iters.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(stat_h, h->status.p, sizeof(int8_t) * P, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->pin.at<char>(os), h->out.p, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
+  if (iters) CK(cudaMemcpyAsync(h->pin.at<char>(oi), h->iters.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->pin.at<char>(ot), h->status.p, sizeof(int8_t) * P, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  std::memcpy(sigma, h->pin.at<char>(os), 8 * (size_t)P);
+  if (iters) std::memcpy(iters, h->pin.at<char>(oi), 4 * (size_t)P);
+  if (status) std::memcpy(status, h->pin.at<char>(ot), (size_t)P);
+  const int8_t* stat_h = h->pin.at<int8_t>(ot);
   return check_status(h, stat_h, nullptr, P, fail_index);
 }
 
@@ -506,54 +532,66 @@ int psb_smin_grid(psb_handle* h, const double* xs, int32_t nx, const double* ys,
   if (!h->have_matrix) return fail(h, PSB_ERR_PARAM, "no matrix set");
   if (!xs || !ys || !sigma || nx < 1 || ny < 1) return fail(h, PSB_ERR_PARAM, "bad grid arguments");
   const int64_t N = (int64_t)nx * ny;
-  // row-major compaction of the region (core.py:204 np.flatnonzero order)
-  std::vector<int64_t> idx;
-  idx.reserve(region ? 0 : N);
-  std::vector<double2> zh;
-  for (int64_t g = 0; g < N; g++) {
-    if (region && !region[g]) continue;
-    idx.push_back(g);
-  }
-  const int64_t P = (int64_t)idx.size();
-  zh.resize(P);
-  for (int64_t t = 0; t < P; t++) {
-    const int64_t g = idx[t];
-    zh[t].x = xs[g % nx];
-    zh[t].y = ys[g / nx];
-  }
   CK(cudaSetDevice(h->device));
   cudaStream_t st = h->stream;
+  // pinned staging: [xs | ys | idx (restricted) | sigma | iters | status]
+  const size_t ox = 0, oy = ox + 8 * (size_t)nx, oidx = oy + 8 * (size_t)ny;
+  const size_t os = oidx + (region ? 8 * (size_t)N : 0), oi = os + 8 * (size_t)N, ot = oi + 4 * (size_t)N;
+  CK(h->pin.ensure(ot + (size_t)N));
+  std::memcpy(h->pin.at<char>(ox), xs, 8 * (size_t)nx);
+  std::memcpy(h->pin.at<char>(oy), ys, 8 * (size_t)ny);
+  // row-major compaction of the region (core.py:204 np.flatnonzero order)
+  int64_t P = N;
+  int64_t* idx = nullptr;
+  if (region) {
+    idx = h->pin.at<int64_t>(oidx);
+    P = 0;
+    for (int64_t g = 0; g < N; g++)
+      if (region[g]) idx[P++] = g;
+  }
   CK(h->out.ensure(sizeof(double) * N));
   CK(h->iters.ensure(sizeof(int32_t) * N));
   CK(h->status.ensure(sizeof(int8_t) * N));
   CK(h->zs.ensure(sizeof(double2) * std::max<int64_t>(P, 1)));
-  CK(h->outidx.ensure(sizeof(int64_t) * std::max<int64_t>(P, 1)));
-  // NaN marks unevaluated points (core.py:203)
-  std::vector<double> nanfill;
-  CK(cudaMemsetAsync(h->out.p, 0xff, sizeof(double) * N, st));  // 0xff.. is a NaN pattern
-  CK(cudaMemsetAsync(h->iters.p, 0, sizeof(int32_t) * N, st));
-  CK(cudaMemsetAsync(h->status.p, 0, sizeof(int8_t) * N, st));
+  CK(h->xs.ensure(8 * (size_t)nx));
+  CK(h->ys.ensure(8 * (size_t)ny));
+  CK(cudaMemcpyAsync(h->xs.p, h->pin.at<char>(ox), 8 * (size_t)nx, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(h->ys.p, h->pin.at<char>(oy), 8 * (size_t)ny, cudaMemcpyHostToDevice, st));
+  const int64_t* d_idx = nullptr;
+  if (region) {
+    // NaN marks unevaluated points (core.py:203); the full grid overwrites every entry
+    CK(cudaMemsetAsync(h->out.p, 0xff, sizeof(double) * N, st));  // 0xff.. is a NaN pattern
+    CK(cudaMemsetAsync(h->iters.p, 0, sizeof(int32_t) * N, st));
+    CK(cudaMemsetAsync(h->status.p, 0, sizeof(int8_t) * N, st));
+    if (P > 0) {
+      CK(h->outidx.ensure(sizeof(int64_t) * P));
+      CK(cudaMemcpyAsync(h->outidx.p, idx, sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
+      d_idx = h->outidx.as<int64_t>();
+    }
+  }
   if (P > 0) {
-    CK(cudaMemcpyAsync(h->zs.p, zh.data(), sizeof(double2) * P, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(h->outidx.p, idx.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
-    int rc = run_pipeline(h, h->zs.as<double2>(), h->outidx.as<int64_t>(), P, h->out.as<double>(),
-                          h->iters.as<int32_t>(), h->status.as<int8_t>(), opts, st);
+    // shifts from the grid axes on the device: z = xs[g % nx] + i ys[g / nx] (the host's linspace bits)
+    k_grid_points<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(h->xs.as<double>(), nx, h->ys.as<double>(), d_idx, P,
+                                                              h->zs.as<double2>());
+    CK(cudaGetLastError());
+    int rc = run_pipeline(h, h->zs.as<double2>(), d_idx, P, h->out.as<double>(), h->iters.as<int32_t>(),
+                          h->status.as<int8_t>(), opts, st);
     if (rc != PSB_OK) return rc;
   } else {
     h->stats = psb_stats{};
   }
-  std::vector<int8_t> stat_local;
-  int8_t* stat_h = status;
-  if (!stat_h) { stat_local.resize(N); stat_h = stat_local.data(); }
-  CK(cudaMemcpyAsync(sigma, h->out.p, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
-  if (iters) CK(cudaMemcpyAsync(iters, h->iters.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(stat_h, h->status.p, sizeof(int8_t) * N, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->pin.at<char>(os), h->out.p, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+  if (iters) CK(cudaMemcpyAsync(h->pin.at<char>(oi), h->iters.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->pin.at<char>(ot), h->status.p, sizeof(int8_t) * N, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  std::memcpy(sigma, h->pin.at<char>(os), 8 * (size_t)N);
+  if (iters) std::memcpy(iters, h->pin.at<char>(oi), 4 * (size_t)N);
+  if (status) std::memcpy(status, h->pin.at<char>(ot), (size_t)N);
   // canonical quiet NaN off-region (the memset pattern is a NaN; normalise for bitwise tests)
   if (region)
     for (int64_t g = 0; g < N; g++)
       if (!region[g]) sigma[g] = std::numeric_limits<double>::quiet_NaN();
-  return check_status(h, stat_h, idx.data(), P, fail_index);
+  return check_status(h, h->pin.at<int8_t>(ot), idx, P, fail_index);
 }
 
 }  // extern "C"
