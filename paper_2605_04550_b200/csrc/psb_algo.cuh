@@ -165,6 +165,7 @@ PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z,
   double2 pre[WM + 1];
 #pragma unroll
   for (int c = 0; c <= WM; c++) pre[c] = (c <= W && kl + 1 < n) ? Ab[(int64_t)c * n + kl + 1] : czero();
+#pragma unroll 2
   for (int j = 0; j < n; j++) {
     // pivot among rows j..j+kl (rows past n are zero and never win a strict '>')
     int p = 0;

@@ -1,2 +1,1 @@
-timeout 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python bench.py --no-cpu-baseline --no-guided 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['e2e'])"
+for c in C2 C3 C4; do timeout 300 python tools/overlap.py $c > /tmp/o.txt 2>&1; head -3 /tmp/o.txt; done

@@ -1,3 +1,8 @@
 set -e
-ncu --set full --clock-control none --import-source on -k regex:"k_lanczos|k_bisect" -c 3 -o gpurun_out/prof_c2b python tools/prof_step.py C2 > gpurun_out/ncu_full.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_bisect" -c 2 -o gpurun_out/prof_c3b python tools/prof_step.py C3 > gpurun_out/ncu_full3.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-guided > gpurun_out/ncu_launch.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_lanczos|k_bisect" -c 3 -o gpurun_out/prof_c2 python tools/prof_step.py C2 > gpurun_out/ncu_full.log 2>&1
+for c in C1 C3 C4 C5; do python bench.py --config $c --no-cpu-baseline --no-guided --steps 3 > gpurun_out/bench_$c.json 2>&1 || true; done
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>&1 || true
