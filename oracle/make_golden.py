@@ -218,6 +218,22 @@ def gen_guided():
     print("c1 guided evals", ne1, "region frac", reg1.mean(), flush=True)
 
 
+def gen_wide():
+    """Larger seeded subsets at SURVEY 8(c)'s sizes: C3 1,024 points (restated; complex A) and
+    C4 256 points (the reference's smin_many; real A)."""
+    for name, count, seed, fn in (("C3", 1024, 32, _restated_chunk), ("C4", 256, 42, _ref_chunk)):
+        cfg = configs.CONFIGS[name]
+        Ad = cfg.matrix().todense()
+        if np.all(Ad.imag == 0):
+            Ad = Ad.real.copy()
+        idx, zs = configs.sample_points(cfg, count, seed)
+        t = time.time()
+        want = _pool(fn, Ad, zs, procs=os.cpu_count() or 8)
+        np.savez_compressed(GOLD / f"{name.lower()}_wide.npz", idx=idx, zs=zs, sigma=want,
+                            norm2=np.linalg.norm(Ad, 2), kind=np.array("reference" if fn is _ref_chunk else "restated"))
+        print(name, "wide", count, time.time() - t, flush=True)
+
+
 def special_field_values():
     """A 6x7 field covering the writer's special cases (exact 0 -> -inf, NaN, inf, subnormal,
     extremes, values needing all 17 digits)."""
@@ -284,6 +300,8 @@ if __name__ == "__main__":
         train_grcar_bundle()
     if what in ("guided", "all"):
         gen_guided()
+    if what == "wide":
+        gen_wide()
     if what in ("io", "all"):
         gen_io()
     if what in ("calib", "all"):

@@ -50,12 +50,16 @@ def test_demo01_golden_including_exact_zeros(gpu, gold):
     masks_agree(fld.values, want, 1.0, [1e-2, 1e-4, 1e-8])
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+@pytest.mark.parametrize("name", ["c2_sample", "c3_sample", "c4_sample", "c3_wide", "c4_wide"])
 def test_config_samples(gpu, gold, name):
-    z = gold(f"{name}_sample.npz")
-    cfg = configs.CONFIGS[name.upper()]
-    got = core.smin_many(cfg.matrix(), z["zs"])
+    """Seeded grid subsets; *_wide are SURVEY 8(c)'s sizes (C3 1,024 points, C4 256)."""
+    z = gold(f"{name}.npz")
+    cfg = configs.CONFIGS[name.split("_")[0].upper()]
+    got, it, st = core.smin_many(cfg.matrix(), z["zs"], return_info=True)
     check(got, z["sigma"], float(z["norm2"]), name)
+    # the points themselves and their engines: batch-invariant (same bits in a different order)
+    perm = np.random.default_rng(0).permutation(got.size)
+    assert np.array_equal(core.smin_many(cfg.matrix(), z["zs"][perm]), got[perm])
 
 
 def test_c5_sample(gpu, gold):

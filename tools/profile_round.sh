@@ -1,3 +1,7 @@
+#!/bin/bash
+# Round profiling recipe (run under gpurun): tests, smoke, bench lines for C1-C5, the reference arm,
+# the ncu launch list of the bench command and one ncu --set full capture of both engines on C2.
+# Summarise with: python tools/ncu_report.py gpurun_out/prof_c2.ncu-rep gpurun_out/launches_c2.csv profiles/rNN_c2_ncu.md /tmp/x.json
 set -e
 timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
