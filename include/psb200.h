@@ -47,7 +47,7 @@ extern "C" {
 typedef struct psb_handle psb_handle;
 
 typedef struct {
-  double tau;          /* engine split: sigma >= tau*(|z|+||A||) -> bisection engine (default 3e-3) */
+  double tau;          /* engine split: sigma >= tau*(|z|+||A||) -> bisection engine (default 8e-4) */
   double bis_rtol;     /* bisection stop: (hi-lo) <= bis_rtol*hi on lambda = sigma^2 (default 2e-12) */
   int32_t kmax;        /* Lanczos step cap (0 -> min(3000, max(64, 4n))) */
   int32_t force_engine;/* 0 auto, 1 Lanczos engine only, 2 bisection engine only (testing) */

@@ -112,8 +112,12 @@ struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np, g; 
 #define KP(KL, KU, NP, G)                                                                               \
   {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, RingDepth<KL, KU>::D>, \
    Ring<KL, KU, RingDepth<KL, KU>::D>::BYTES, NP, G}
+#ifdef PSB_DEV_SHAPES  // development builds only (faster compiles): the BASELINE config shapes
+static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 3, 2, 1), KP(3, 3, 2, 1)};
+#else
 static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 2, 2, 1), KP(2, 3, 2, 1), KP(3, 3, 2, 1),
                                KP(4, 4, 1, 1), KP(1, 2, 2, 1), KP(2, 1, 2, 1)};
+#endif
 static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,
                            &k_lanczos<16, 16, true, 2>, 0, 1, 1};
 static KPair pick(int kl, int ku) {
@@ -291,7 +295,7 @@ static double bytes_it_row(int kl, int ku) {
 static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_outidx, int64_t P, double* d_out,
                         int32_t* d_iters, int8_t* d_status, const psb_opts* o, cudaStream_t st) {
   psb_opts opt{};
-  opt.tau = 3e-3; opt.bis_rtol = 2e-12; opt.kmax = 0; opt.force_engine = 0; opt.refill = 16;
+  opt.tau = 8e-4; opt.bis_rtol = 2e-12; opt.kmax = 0; opt.force_engine = 0; opt.refill = 16;
   if (o) {
     if (o->tau > 0) opt.tau = o->tau;
     if (o->bis_rtol > 0) opt.bis_rtol = o->bis_rtol;
@@ -438,8 +442,10 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   if (h->k_prof && nA_run > 0) {
     unsigned long long pr[8];
     cudaMemcpy(pr, h->prof.p, 64, cudaMemcpyDeviceToHost);
-    fprintf(stderr, "[psb prof] warp-cycles: lu %.3g s1 %.3g s2 %.3g s3 %.3g s4 %.3g ritz %.3g (gridL %lld)\n",
-            (double)pr[0], (double)pr[1], (double)pr[2], (double)pr[3], (double)pr[4], (double)pr[5], (long long)gridL);
+    fprintf(stderr, "[psb prof] warp-cycles: lu %.3g s1 %.3g s2 %.3g s3 %.3g s4 %.3g ritz %.3g (gridL %lld) "
+            "lane-occupancy of step iterations %.3f over %llu warp-steps\n",
+            (double)pr[0], (double)pr[1], (double)pr[2], (double)pr[3], (double)pr[4], (double)pr[5], (long long)gridL,
+            pr[7] ? (double)pr[6] / (32.0 * (double)pr[7]) : 0.0, pr[7]);
   }
   psb_stats& S = h->stats;
   S.n_bisect = (int64_t)hc[3];

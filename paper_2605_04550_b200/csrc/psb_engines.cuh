@@ -554,8 +554,11 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         lo = nlo;  // every probe PD: keep searching upward
       } else {
         phase = 2;
-        if (nlo >= nhi) {  // non-monotone answers: the decision is at the rounding level here
-          lo = hi = 0.5 * (lo + (hi == INFINITY ? phi : hi));
+        if (nlo >= nhi) {
+          // Non-monotone answers: a PD probe above a non-PD one, so both sit inside the rounding band
+          // of sigma_min^2 and the answer is their midpoint. (Not the old bracket's: a secant probe
+          // lands in that band while the bracket is still wide.)
+          lo = hi = 0.5 * (nlo + nhi);
           r = BIS_DONE;
         } else {
           lo = nlo;
@@ -684,6 +687,7 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       if (exhausted && __ballot_sync(FULL, phase != 0) == 0) break;
       continue;
     }
+    if (a.prof && lane == 0) { atomicAdd(&a.prof[6], (unsigned long long)__popc(act)); atomicAdd(&a.prof[7], 1ull); }
     if (phase == 2 && s1done) {
       s1done = false;
     } else if (phase == 2) {
