@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/psb200.h"
-#include "psb_engines.cuh"
+#include "psb_dispatch.cuh"
 #include "psb_predict.cuh"
 
 using namespace psb;
@@ -100,30 +100,38 @@ static int fail(psb_handle* h, int code, const std::string& msg) {
                                        " at " #call);                                     \
   } while (0)
 
+namespace psb {
+// Grid shifts on the device: point t is grid index g = idx[t] (or t), z = xs[g % nx] + i ys[g / nx].
+// xs / ys are the host's linspace values, so z carries exactly the reference's bits (core.py:70-78).
+__global__ void k_grid_points(const double* __restrict__ xs, int nx, const double* __restrict__ ys,
+                              const int64_t* __restrict__ idx, int64_t P, double2* __restrict__ zs) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P) return;
+  const int64_t g = idx ? idx[t] : t;
+  zs[t] = make_double2(xs[g % nx], ys[g / nx]);
+}
+
+}  // namespace psb
+
 // ----------------------------------------------------------------------------- dispatch
-// Exact-shape instantiations (the BASELINE configs and the reference's random banded
-// ensemble beta in 1..4, generate.py:42-69); every other band up to 16/16 runs the
-// runtime-shape (DYN) instantiation.
-typedef void (*bis_fn)(BisArgs);
-typedef void (*lan_fn)(LanArgs);
-// b: classification (NP = 1); bm: multisection (NP probes per thread); l: Lanczos engine.
-struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np, g; };  // lsmem: per warp
-// (NP probes per lane) x (G lanes per point), fixed per band shape (results must not depend on the batch)
-#define KP(KL, KU, NP, G)                                                                               \
-  {KL, KU, &k_bisect<KL, KU, false, 1, 1>, &k_bisect<KL, KU, false, NP, G>, &k_lanczos<KL, KU, false, RingDepth<KL, KU>::D>, \
-   Ring<KL, KU, RingDepth<KL, KU>::D>::BYTES, NP, G}
-#ifdef PSB_DEV_SHAPES  // development builds only (faster compiles): the BASELINE config shapes
-static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 3, 2, 1), KP(3, 3, 2, 1)};
-#else
-static const KPair kTable[] = {KP(1, 1, 2, 1), KP(1, 3, 2, 1), KP(2, 2, 2, 1), KP(2, 3, 2, 1), KP(3, 3, 2, 1),
-                               KP(4, 4, 1, 1), KP(1, 2, 2, 1), KP(2, 1, 2, 1)};
-#endif
-static const KPair kDyn = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,
-                           &k_lanczos<16, 16, true, 2>, 0, 1, 1};
-static KPair pick(int kl, int ku) {
-  for (const KPair& k : kTable)
-    if (k.kl == kl && k.ku == ku) return k;
-  return kDyn;
+// Exact-shape kernel sets (the BASELINE configs and the reference's random banded ensemble
+// beta in 1..4, generate.py:42-69) register themselves from their own translation units
+// (psb_shape.cu); every other band up to 16/16 runs the runtime-shape (DYN) set.
+static std::vector<KPair>& shape_registry() {
+  static std::vector<KPair> r;
+  return r;
+}
+void psb::register_shape(const KPair& k) { shape_registry().push_back(k); }
+
+static bool pick(int kl, int ku, KPair* out) {
+  const KPair* dyn = nullptr;
+  for (const KPair& k : shape_registry()) {
+    if (k.kl == kl && k.ku == ku) { *out = k; return true; }
+    if (k.kl < 0) dyn = &k;
+  }
+  if (!dyn) return false;
+  *out = *dyn;
+  return true;
 }
 
 static int default_kmax(int n) { return std::min(3000, std::max(64, 4 * n)); }
@@ -305,7 +313,8 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   }
   const int n = h->n, kl = h->kl, ku = h->ku;
   const int kmax = opt.kmax > 0 ? opt.kmax : default_kmax(n);
-  const KPair kp = pick(kl, ku);
+  KPair kp;
+  if (!pick(kl, ku, &kp)) return fail(h, PSB_ERR_CUDA, "library built without a kernel set for this band shape");
   const bool dyn = kp.kl < 0;
   h->stats = psb_stats{};
   h->stats.n_points = P;

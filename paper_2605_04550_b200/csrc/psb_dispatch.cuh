@@ -1,0 +1,21 @@
+// psb_dispatch.cuh — per-band-shape kernel sets and their registry.
+//
+// Each exact band shape (kl, ku) is compiled in its own translation unit (psb_shape.cu built once
+// per shape with -DPSB_KL/-DPSB_KU/-DPSB_NP/-DPSB_G, or -DPSB_DYN for the runtime-shape set), so
+// the library builds in parallel. Every unit registers its kernel set at load time; the C ABI picks
+// the exact-shape set for the matrix's band or falls back to the runtime-shape one.
+#pragma once
+#include "psb_engines.cuh"
+
+namespace psb {
+
+typedef void (*bis_fn)(BisArgs);
+typedef void (*lan_fn)(LanArgs);
+// b: classification (NP = 1); bm: multisection (NP probes per thread); l: Lanczos engine.
+// (NP probes per lane) x (G lanes per point) are fixed per band shape: results must not depend on
+// the batch. lsmem: Lanczos ring bytes per warp. kl = -1 marks the runtime-shape set.
+struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np, g; };
+
+void register_shape(const KPair& k);  // defined in psb_capi.cu
+
+}  // namespace psb

@@ -313,16 +313,6 @@ struct RingDepth {
 
 __device__ __forceinline__ int64_t out_index(const int64_t* outidx, int64_t p) { return outidx ? outidx[p] : p; }
 
-// Grid shifts on the device: point t is grid index g = idx[t] (or t), z = xs[g % nx] + i ys[g / nx].
-// xs / ys are the host's linspace values, so z carries exactly the reference's bits (core.py:70-78).
-__global__ void k_grid_points(const double* __restrict__ xs, int nx, const double* __restrict__ ys,
-                              const int64_t* __restrict__ idx, int64_t P, double2* __restrict__ zs) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= P) return;
-  const int64_t g = idx ? idx[t] : t;
-  zs[t] = make_double2(xs[g % nx], ys[g / nx]);
-}
-
 // ----------------------------------------------------------------- engine B kernel
 // mode 0 (NP = G = 1): classification — one LDL^H test per point at lambda = (tau S)^2; PD points
 //   go to listB (sigma >= tau S), the rest to listA (Lanczos engine).

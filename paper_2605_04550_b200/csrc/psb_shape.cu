@@ -1,0 +1,24 @@
+// psb_shape.cu — one band shape's kernel set (see psb_dispatch.cuh). Compiled once per exact
+// shape with -DPSB_KL=.. -DPSB_KU=.. -DPSB_NP=.. -DPSB_G=.., and once with -DPSB_DYN for the
+// runtime-shape instantiation (any band up to 16/16).
+#include "psb_dispatch.cuh"
+
+namespace psb {
+namespace {
+
+#ifdef PSB_DYN
+const KPair kSet = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,
+                    &k_lanczos<16, 16, true, 2>, 0, 1, 1};
+#else
+constexpr int D = RingDepth<PSB_KL, PSB_KU>::D;
+const KPair kSet = {PSB_KL, PSB_KU, &k_bisect<PSB_KL, PSB_KU, false, 1, 1>,
+                    &k_bisect<PSB_KL, PSB_KU, false, PSB_NP, PSB_G>, &k_lanczos<PSB_KL, PSB_KU, false, D>,
+                    Ring<PSB_KL, PSB_KU, D>::BYTES, PSB_NP, PSB_G};
+#endif
+
+struct Registrar {
+  Registrar() { register_shape(kSet); }
+} registrar;
+
+}  // namespace
+}  // namespace psb

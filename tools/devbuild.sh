@@ -1,7 +1,6 @@
 #!/bin/bash
-# Development build: only the BASELINE config band shapes (PSB_DEV_SHAPES), for faster A/B iterations.
-# The product build is __graft_entry__.build().
+# Development build: only the BASELINE config band shapes, for faster A/B iterations.
+# The product build is __graft_entry__.build() (every shape).
 set -e
 cd "$(dirname "$0")/.."
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
-  -DPSB_DEV_SHAPES "$@" -o paper_2605_04550_b200/libpsb200.so paper_2605_04550_b200/csrc/psb_capi.cu paper_2605_04550_b200/csrc/psb_io.cpp
+PSB_BUILD_KEEP_DYN=1 PSB_BUILD_SHAPES="1,1,2,1;1,3,2,1;2,3,2,1;3,3,2,1" python -c "import __graft_entry__ as g; g.build(force=True)"
