@@ -441,8 +441,8 @@ PSB_HD bool lanczos_converged(double theta, double dtheta, double r, double beta
 }
 
 // --------------------------------------------------------- engine B: PD test
-// Is G(lam) = A^H A - conj(z) A - z A^H + (|z|^2 - lam) I positive definite?
-// AHA[d * n + j] = (A^H A)[j, j-d], d = 0..b, b = kl + ku.
+// Is G(lam) = M^H M - lam I, M = zI - A, positive definite? G's band (b = kl + ku) is formed
+// row by row from M's entries (g_entry); the diagonal shift is zz = -lam.
 // Left-looking banded LDL^H; the previous b rows of L live in a ring of b register
 // slots (row j in slot j mod b; the row loop is unrolled by b so every slot index is a
 // compile-time constant). Virtual rows before 0 are L = 0, D = 1.
@@ -453,19 +453,26 @@ struct PDRing {
   double D[B], iD[B];
 };
 
+// M = zI - A from the band: M[k, k+e] = (e == 0 ? z : 0) - A[k, k+e], e in [-KL, KU].
+PSB_HD double2 m_entry(const double2* __restrict__ Ab, int n, int kl, int k, int e, double2 z) {
+  const double2 a = Ab[(int64_t)(kl + e) * n + k];
+  return (e == 0) ? csub(z, a) : cmk(-a.x, -a.y);
+}
+
+// G[j, j-d] = (M^H M)[j, j-d] = sum_k conj(M[k, j]) M[k, j-d] over k in [j-KU, j-d+KL] (within [0, n)).
+// Formed from M's own entries, so its rounding is relative to M's column norms (the scale T(z) of the
+// engine split), not to (|z| + ||A||)^2 as the expansion A^H A - conj(z) A - z A^H + |z|^2 I would be.
 template <int KLM, int KUM>
-PSB_HD double2 g_entry(int n, int j, int d, const double2* __restrict__ Ab, const double2* __restrict__ AHA,
-                       double2 z, double zz) {
-  double2 v = AHA[(int64_t)d * n + j];
-  if (d <= KLM) {  // - conj(z) * A[j, j-d]
-    double2 a = Ab[(int64_t)(KLM - d) * n + j];
-    v = cfms_cj(v, z, a);
+PSB_HD double2 g_entry(int n, int j, int d, const double2* __restrict__ Ab, double2 z) {
+  double2 v = czero();
+#pragma unroll
+  for (int t = 0; t <= KLM + KUM - d; t++) {
+    const int k = j - KUM + t;
+    if (k < 0 || k >= n) continue;
+    const double2 m1 = m_entry(Ab, n, KLM, k, KUM - t, z);      // M[k, j]
+    const double2 m2 = m_entry(Ab, n, KLM, k, KUM - t - d, z);  // M[k, j-d]
+    v = cfms_cj(v, cmk(-m1.x, -m1.y), m2);
   }
-  if (d <= KUM) {  // - z * conj(A[j-d, j])
-    double2 a = Ab[(int64_t)(KLM + d) * n + (j - d)];
-    v = cfms(v, z, cconj(a));
-  }
-  if (d == 0) v.x += zz;
   return v;
 }
 
@@ -473,11 +480,11 @@ PSB_HD double2 g_entry(int n, int j, int d, const double2* __restrict__ Ab, cons
 // the off-diagonal G entries (only the diagonal depends on lambda). U = j mod B (compile-time).
 template <int KLM, int KUM, int NP, int U>
 PSB_HD void pd_row(PDRing<KLM, KUM> (&R)[NP], int n, int j, const double2* __restrict__ Ab,
-                   const double2* __restrict__ AHA, double2 z, const double (&zz)[NP], bool (&pd)[NP]) {
+                   double2 z, const double (&zz)[NP], bool (&pd)[NP]) {
   constexpr int B = KLM + KUM;
   double2 g[B + 1];
 #pragma unroll
-  for (int d = 0; d <= B; d++) g[d] = (j - d >= 0) ? g_entry<KLM, KUM>(n, j, d, Ab, AHA, z, 0.0) : czero();
+  for (int d = 0; d <= B; d++) g[d] = (j - d >= 0) ? g_entry<KLM, KUM>(n, j, d, Ab, z) : czero();
 #pragma unroll
   for (int q = 0; q < NP; q++) {
     double2 Lj[B + 1], LD[B + 1];
@@ -503,17 +510,17 @@ PSB_HD void pd_row(PDRing<KLM, KUM> (&R)[NP], int n, int j, const double2* __res
 
 template <int KLM, int KUM, int NP, int U>
 struct PDUnroll {
-  PSB_HD static void run(PDRing<KLM, KUM> (&R)[NP], int n, int jb, const double2* Ab, const double2* AHA,
+  PSB_HD static void run(PDRing<KLM, KUM> (&R)[NP], int n, int jb, const double2* Ab, 
                          double2 z, const double (&zz)[NP], bool (&pd)[NP]) {
     if (jb + U < n) {
-      pd_row<KLM, KUM, NP, U>(R, n, jb + U, Ab, AHA, z, zz, pd);
-      PDUnroll<KLM, KUM, NP, U + 1>::run(R, n, jb, Ab, AHA, z, zz, pd);
+      pd_row<KLM, KUM, NP, U>(R, n, jb + U, Ab, z, zz, pd);
+      PDUnroll<KLM, KUM, NP, U + 1>::run(R, n, jb, Ab, z, zz, pd);
     }
   }
 };
 template <int KLM, int KUM, int NP>
 struct PDUnroll<KLM, KUM, NP, KLM + KUM> {
-  PSB_HD static void run(PDRing<KLM, KUM> (&)[NP], int, int, const double2*, const double2*, double2,
+  PSB_HD static void run(PDRing<KLM, KUM> (&)[NP], int, int, const double2*, double2,
                          const double (&)[NP], bool (&)[NP]) {}
 };
 
@@ -530,14 +537,14 @@ struct PDWin {
 
 template <int KLM, int KUM, int NP>
 PSB_HD void pdw_load_row(PDWin<KLM, KUM> (&Wn)[NP], int r, int n, int i, const double2* __restrict__ Ab,
-                         const double2* __restrict__ AHA, double2 z, const double (&zz)[NP]) {
+                         double2 z, const double (&zz)[NP]) {
   // row r of the window = matrix row i, columns i-r .. i (G entries G[i, i-d], d = r - c)
   constexpr int B = KLM + KUM;
   double2 g[B + 1];
 #pragma unroll
   for (int d = 0; d <= B; d++) {
     g[d] = czero();
-    if (d <= r && i < n && i - d >= 0) g[d] = g_entry<KLM, KUM>(n, i, d, Ab, AHA, z, 0.0);
+    if (d <= r && i < n && i - d >= 0) g[d] = g_entry<KLM, KUM>(n, i, d, Ab, z);
   }
 #pragma unroll
   for (int q = 0; q < NP; q++) {
@@ -618,21 +625,21 @@ PSB_HD void pdw_step(PDWin<KLM, KUM> (&Wn)[NP], bool (&pd)[NP], LogDet (&ld)[NP]
 
 // Whole PD test (right-looking) for NP shifts; `vote` lets device callers exit early.
 template <int KLM, int KUM, int NP>
-PSB_HD void pdw_test(int n, const double2* __restrict__ Ab, const double2* __restrict__ AHA, double2 z,
+PSB_HD void pdw_test(int n, const double2* __restrict__ Ab, double2 z,
                      const double (&lam)[NP], bool (&pd)[NP]) {
   constexpr int B = KLM + KUM;
   PDWin<KLM, KUM> Wn[NP];
   double zz[NP];
 #pragma unroll
-  for (int q = 0; q < NP; q++) { zz[q] = cnorm2(z) - lam[q]; pd[q] = true; }
+  for (int q = 0; q < NP; q++) { zz[q] = -lam[q]; pd[q] = true; }
   LogDet ld[NP];
 #pragma unroll
   for (int q = 0; q < NP; q++) ld[q].init();
 #pragma unroll
-  for (int r = 0; r <= B; r++) pdw_load_row<KLM, KUM, NP>(Wn, r, n, r, Ab, AHA, z, zz);
+  for (int r = 0; r <= B; r++) pdw_load_row<KLM, KUM, NP>(Wn, r, n, r, Ab, z, zz);
   for (int j = 0; j < n; j++) {
     pdw_step<KLM, KUM, NP>(Wn, pd, ld);
-    pdw_load_row<KLM, KUM, NP>(Wn, B, n, j + 1 + B, Ab, AHA, z, zz);
+    pdw_load_row<KLM, KUM, NP>(Wn, B, n, j + 1 + B, Ab, z, zz);
     if ((j & 15) == 15)
       for (int q = 0; q < NP; q++) ld[q].norm();
   }
@@ -653,29 +660,35 @@ PSB_HD void pd_init(PDRing<KLM, KUM>& R) {
 // Host/generic form: whole-test loop (device kernels drive the group loop themselves so
 // they can vote on early exit).
 template <int KLM, int KUM>
-PSB_HD bool pd_test_static(int n, const double2* __restrict__ Ab, const double2* __restrict__ AHA, double2 z,
+PSB_HD bool pd_test_static(int n, const double2* __restrict__ Ab, double2 z,
                            double lam) {
   constexpr int B = KLM + KUM;
   PDRing<KLM, KUM> R[1];
   pd_init(R[0]);
-  const double zz[1] = {cnorm2(z) - lam};
+  const double zz[1] = {-lam};
   bool pd[1] = {true};
-  for (int jb = 0; jb < n && pd[0]; jb += B) PDUnroll<KLM, KUM, 1, 0>::run(R, n, jb, Ab, AHA, z, zz, pd);
+  for (int jb = 0; jb < n && pd[0]; jb += B) PDUnroll<KLM, KUM, 1, 0>::run(R, n, jb, Ab, z, zz, pd);
   return pd[0];
 }
 
 // Runtime-shape PD test (any kl, ku; ring in a caller-provided scratch of b*b complex + 2b doubles).
-PSB_HD bool pd_test_dyn(int n, int kl, int ku, const double2* __restrict__ Ab, const double2* __restrict__ AHA,
+PSB_HD bool pd_test_dyn(int n, int kl, int ku, const double2* __restrict__ Ab,
                         double2 z, double lam, LV Lsc, double* Dsc, int dld) {
   const int b = kl + ku;
-  const double zz = cnorm2(z) - lam;
-  if (b == 0) {  // diagonal A
-    for (int j = 0; j < n; j++) {
-      double2 v = AHA[j];
-      v = cfms_cj(v, z, Ab[j]);
-      v = cfms(v, z, cconj(Ab[j]));
-      if (!(v.x + zz > 0.0)) return false;
+  // G[j, j-d] from M's entries (see g_entry)
+  auto gent = [&](int j, int d) {
+    double2 v = czero();
+    for (int t = 0; t <= b - d; t++) {
+      const int k = j - ku + t;
+      if (k < 0 || k >= n) continue;
+      const double2 m1 = m_entry(Ab, n, kl, k, ku - t, z), m2 = m_entry(Ab, n, kl, k, ku - t - d, z);
+      v = cfms_cj(v, cmk(-m1.x, -m1.y), m2);
     }
+    return v;
+  };
+  if (b == 0) {  // diagonal A
+    for (int j = 0; j < n; j++)
+      if (!(gent(j, 0).x - lam > 0.0)) return false;
     return true;
   }
   for (int s = 0; s < b; s++) {
@@ -687,22 +700,14 @@ PSB_HD bool pd_test_dyn(int n, int kl, int ku, const double2* __restrict__ Ab, c
   for (int j = 0; j < n; j++) {
     for (int d = b; d >= 1; d--) {
       const int c = j - d;
-      double2 g = czero();
-      if (c >= 0) {
-        g = AHA[(int64_t)d * n + j];
-        if (d <= kl) g = cfms_cj(g, z, Ab[(int64_t)(kl - d) * n + j]);
-        if (d <= ku) g = cfms(g, z, cconj(Ab[(int64_t)(kl + d) * n + c]));
-      }
+      const double2 g = (c >= 0) ? gent(j, d) : czero();
       const int sc = ((c % b) + b) % b;
       double2 sacc = g;
       for (int dm = b; dm > d; dm--) sacc = cfms_cj(sacc, Lsc.get((int64_t)sc * b + dm - d - 1), LD[dm]);
       Lj[d] = cscale(sacc, Dsc[(int64_t)(2 * sc + 1) * dld]);
       LD[d] = cscale(Lj[d], Dsc[(int64_t)(2 * sc) * dld]);
     }
-    double2 g0 = AHA[j];
-    g0 = cfms_cj(g0, z, Ab[(int64_t)kl * n + j]);
-    g0 = cfms(g0, z, cconj(Ab[(int64_t)kl * n + j]));
-    double dj = g0.x + zz;
+    double dj = gent(j, 0).x - lam;
     for (int d = 1; d <= b; d++) dj -= cdotr(Lj[d], LD[d]);
     if (!(dj > 0.0)) return false;
     const int s0 = j % b;

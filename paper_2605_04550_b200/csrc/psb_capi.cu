@@ -69,16 +69,18 @@ struct psb_handle {
   std::mutex mu;
   // matrix
   int n = 0, kl = 0, ku = 0;
-  double anorm = 0.0;
+  double2 dc{0.0, 0.0};  // engine-split scale (BisArgs): disc of A's diagonal, max off-diagonal column norm^2
+  double dr = 0.0, offsq = 0.0;
   int tz_j0 = 1, tz_j1 = 0;  // interior rows sharing one G row (diagonal-constant band), empty by default
   // development knobs, read once at psb_create (A/B switches; defaults are the product path):
-  //   PSB_NOSEC=1 plain multisection, PSB_NOTZ=1 per-row G formation, PSB_LWARPS=N cap on
+  //   PSB_TAU=x default engine split, PSB_BTPB=n engine-B block size, PSB_NOSEC=1 plain multisection, PSB_NOTZ=1 per-row G formation, PSB_LWARPS=N cap on
   //   Lanczos warps, PSB_PROF=1 per-phase clock64 counters of the Lanczos kernel (stderr)
   bool k_secant = true, k_toeplitz = true, k_prof = false;
   long long k_lwarps = 0;
   int k_btpb = 128;
+  double k_tau = 0.0;
   bool have_matrix = false;
-  DevBuf Ab, AHA, v1;
+  DevBuf Ab, v1, offmin, gbuf;
   // per call
   DevBuf zs, outidx, out, iters, status, listA, listB, counters, scratch, pivs, dynL, dynD;
   DevBuf xs, ys, prof;
@@ -154,7 +156,8 @@ int psb_create(int device, psb_handle** out) {
   h->k_secant = getenv("PSB_NOSEC") == nullptr;
   h->k_toeplitz = getenv("PSB_NOTZ") == nullptr;
   h->k_prof = getenv("PSB_PROF") != nullptr;
-  h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 128;
+  h->k_tau = getenv("PSB_TAU") ? atof(getenv("PSB_TAU")) : 0.0;  // dev: default engine split
+  h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 0;  // 0: pick per launch
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
@@ -166,7 +169,7 @@ int psb_create(int device, psb_handle** out) {
 void psb_destroy(psb_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->v1, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
+  DevBuf* bufs[] = {&h->Ab, &h->v1, &h->offmin, &h->gbuf, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
                     &h->counters, &h->scratch, &h->pivs, &h->dynL, &h->dynD, &h->xs, &h->ys, &h->params,
                     &h->feat, &h->eig, &h->prob, &h->region, &h->idx};
   for (DevBuf* b : bufs) b->release();
@@ -206,27 +209,37 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
     if (d < -kl || d > ku || i < 0 || c < 0 || i >= n || c >= n) return cd(0, 0);
     return A[(int64_t)(d + kl) * n + i];
   };
-  // A^H A band: AHA[d*n + j] = (A^H A)[j, j-d] = sum_k conj(A[k, j]) A[k, j-d]
   const int b = kl + ku;
-  std::vector<cd> aha((size_t)(b + 1) * n, cd(0, 0));
-  for (int j = 0; j < n; j++)
-    for (int d = 0; d <= b && j - d >= 0; d++) {
-      const int c = j - d;
-      cd s(0, 0);
-      for (int k = std::max(0, j - ku); k <= std::min(n - 1, c + kl); k++) s += std::conj(Aat(k, j)) * Aat(k, c);
-      aha[(size_t)d * n + j] = s;
-    }
-  // ||A||_2 <= sqrt(||A||_1 ||A||_inf)
-  std::vector<double> colsum(n, 0.0), rowsum(n, 0.0);
-  for (int d = -kl; d <= ku; d++)
+  CK(cudaSetDevice(h->device));
+  // Engine-split scale T(z)^2 = (|z - dc| + dr)^2 + offsq bounds every column norm^2 of M = zI - A:
+  // |M[j,j]| = |z - a_jj| <= |z - dc| + dr, and the off-diagonal part of column j is z-independent.
+  {
+    double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
     for (int i = 0; i < n; i++) {
-      if (i + d < 0 || i + d >= n) continue;
-      double m = std::abs(A[(int64_t)(d + kl) * n + i]);
-      rowsum[i] += m;
-      colsum[i + d] += m;
+      const cd a = A[(int64_t)kl * n + i];
+      xmin = std::min(xmin, a.real()); xmax = std::max(xmax, a.real());
+      ymin = std::min(ymin, a.imag()); ymax = std::max(ymax, a.imag());
     }
-  double n1 = *std::max_element(colsum.begin(), colsum.end());
-  double ni = *std::max_element(rowsum.begin(), rowsum.end());
+    const cd c(0.5 * (xmin + xmax), 0.5 * (ymin + ymax));
+    double r = 0.0;
+    for (int i = 0; i < n; i++) r = std::max(r, std::abs(A[(int64_t)kl * n + i] - c));
+    std::vector<double> off(n, 0.0), offr(n, 0.0);
+    for (int d = -kl; d <= ku; d++) {
+      if (d == 0) continue;
+      for (int i = 0; i < n; i++)
+        if (i + d >= 0 && i + d < n) {
+          off[i + d] += std::norm(A[(int64_t)(d + kl) * n + i]);
+          offr[i] += std::norm(A[(int64_t)(d + kl) * n + i]);
+        }
+    }
+    std::vector<double> om(n);
+    for (int i = 0; i < n; i++) om[i] = std::min(off[i], offr[i]);
+    CK(h->offmin.ensure(sizeof(double) * n));
+    CK(cudaMemcpy(h->offmin.p, om.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    h->dc = make_double2(c.real(), c.imag());
+    h->dr = r * (1.0 + 1e-15);
+    h->offsq = *std::max_element(off.begin(), off.end()) * (1.0 + 1e-15);
+  }
   // Lanczos start vector: fixed, identical for every z (determinism)
   std::vector<cd> v1(n);
   double nrm = 0.0;
@@ -238,10 +251,8 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
   for (auto& v : v1) v /= nrm;
   CK(cudaSetDevice(h->device));
   CK(h->Ab.ensure(sizeof(cd) * nd * n));
-  CK(h->AHA.ensure(sizeof(cd) * (b + 1) * n));
   CK(h->v1.ensure(sizeof(cd) * n * 33));
   CK(cudaMemcpyAsync(h->Ab.p, band, sizeof(cd) * nd * n, cudaMemcpyHostToDevice, h->stream));
-  CK(cudaMemcpyAsync(h->AHA.p, aha.data(), sizeof(cd) * (b + 1) * n, cudaMemcpyHostToDevice, h->stream));
   // [0, n): v1; [n, 33n): v1 replicated per lane (v1rep[j*32 + lane]) for coalesced cp.async
   std::vector<cd> v1x((size_t)n * 33);
   for (int i = 0; i < n; i++) {
@@ -251,17 +262,19 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
   CK(cudaMemcpyAsync(h->v1.p, v1x.data(), sizeof(cd) * n * 33, cudaMemcpyHostToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   h->n = n; h->kl = kl; h->ku = ku;
-  h->anorm = std::sqrt(n1 * ni);
-  // Rows whose G(lambda) row entries are bitwise identical (every band diagonal constant there and
-  // all terms of A^H A present): the bisection engine forms that row once per test. The values are
-  // the same numbers the per-row path would load, so results do not change.
+  // Rows whose G(lambda) row entries are bitwise identical: G row j is formed from A's rows
+  // [j - ku, j + kl] (g_entry), so rows j whose whole window matches row m's window entry for entry
+  // share one G row; the bisection engine forms it once per test. The values are the same numbers
+  // the per-row path would form, so results do not change.
   {
+    auto same_arow = [&](int i, int m) {
+      for (int e = -kl; e <= ku; e++)
+        if (A[(int64_t)(e + kl) * n + i] != A[(int64_t)(e + kl) * n + m]) return false;
+      return true;
+    };
     auto same_row = [&](int i, int m) {
-      for (int d = 0; d <= b; d++) {
-        if (aha[(size_t)d * n + i] != aha[(size_t)d * n + m]) return false;
-        if (d <= kl && A[(int64_t)(kl - d) * n + i] != A[(int64_t)(kl - d) * n + m]) return false;
-        if (d <= ku && A[(int64_t)(kl + d) * n + (i - d)] != A[(int64_t)(kl + d) * n + (m - d)]) return false;
-      }
+      for (int o = -ku; o <= kl; o++)
+        if (!same_arow(i + o, m + o)) return false;
       return true;
     };
     const int m = n / 2;
@@ -283,9 +296,10 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
 // One right-looking LDL^H row per probe: b column scalings (2 flops), b(b-1)/2 off-diagonal complex
 // updates (8), b diagonal updates (4), one reciprocal (1) -> 4b^2 + 2b + 1.
 static double flops_ldl_row(int kl, int ku) { const double b = kl + ku; return 4.0 * b * b + 2.0 * b + 1.0; }
-// Forming one G row: b+1 entries AHA - conj(z) A_low - z conj(A_up) (+ the diagonal shift); shared by
-// the probes of a round, and formed once per round for the interior rows of a diagonal-constant band.
-static double flops_g_row(int kl, int ku) { return 8.0 * (kl + 1) + 8.0 * (ku + 1) + 2.0; }
+// Forming one G row from M = zI - A: entry d is a sum of b - d + 1 products conj(M[k,j]) M[k,j-d]
+// (8 flops each) -> 4 (b+1)(b+2) + 2 (the two diagonals of M); shared by the probes of a round, and
+// formed once per round for the interior rows of a diagonal-constant band.
+static double flops_g_row(int kl, int ku) { const double b = kl + ku; return 4.0 * (b + 1) * (b + 2) + 2.0; }
 static double flops_lu_row(int kl, int ku) { const int W = kl + ku; return 6.0 * W + 6.0 + kl * (6.0 + 8.0 * W); }
 static double flops_it_row(int kl, int ku) {
   const int W = kl + ku;
@@ -303,7 +317,7 @@ static double bytes_it_row(int kl, int ku) {
 static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_outidx, int64_t P, double* d_out,
                         int32_t* d_iters, int8_t* d_status, const psb_opts* o, cudaStream_t st) {
   psb_opts opt{};
-  opt.tau = 8e-4; opt.bis_rtol = 2e-12; opt.kmax = 0; opt.force_engine = 0; opt.refill = 16;
+  opt.tau = h->k_tau > 0 ? h->k_tau : 1.5e-3; opt.bis_rtol = 2e-12; opt.kmax = 0; opt.force_engine = 0; opt.refill = 16;
   if (o) {
     if (o->tau > 0) opt.tau = o->tau;
     if (o->bis_rtol > 0) opt.bis_rtol = o->bis_rtol;
@@ -316,6 +330,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   KPair kp;
   if (!pick(kl, ku, &kp)) return fail(h, PSB_ERR_CUDA, "library built without a kernel set for this band shape");
   const bool dyn = kp.kl < 0;
+  if (!dyn && h->tz_j0 <= h->tz_j1 && h->k_toeplitz) { kp.b = kp.bt; kp.bm = kp.bmt; }  // diagonal-constant row loop
   h->stats = psb_stats{};
   h->stats.n_points = P;
   if (P == 0) return PSB_OK;
@@ -332,9 +347,9 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   occB = std::max(occB, 1);
   BisArgs ba;
   ba.n = n; ba.kl = kl; ba.ku = ku;
-  ba.Ab = h->Ab.as<double2>(); ba.AHA = h->AHA.as<double2>();
+  ba.Ab = h->Ab.as<double2>(); ba.offmin = h->offmin.as<double>();
   ba.zs = d_zs; ba.outidx = d_outidx; ba.P = P;
-  ba.anorm = h->anorm; ba.tau = opt.tau; ba.rtol = opt.bis_rtol;
+  ba.dc = h->dc; ba.dr = h->dr; ba.offsq = h->offsq; ba.tau = opt.tau; ba.rtol = opt.bis_rtol;
   ba.force = opt.force_engine; ba.max_tests = 400;
   ba.out = d_out; ba.iters = d_iters; ba.status = d_status;
   ba.listA = h->listA.as<int64_t>(); ba.listB = h->listB.as<int64_t>(); ba.counters = cnt;
@@ -352,6 +367,15 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     CK(h->dynD.ensure(sizeof(double) * threads * 2 * b));
     ba.dyn_L = h->dynL.as<double2>(); ba.dyn_D = h->dynD.as<double>();
   }
+  ba.gb = nullptr; ba.nb = 0; ba.gb_T = 0;
+  const bool tzk = !dyn && h->tz_j0 <= h->tz_j1 && h->k_toeplitz;
+  if (tzk) {
+    // per-thread G-row slots of the TZ kernels; any persistent grid has <= 2048 threads per SM
+    ba.nb = h->tz_j0 + (n - 1 - h->tz_j1);
+    CK(h->gbuf.ensure(sizeof(double2) * (size_t)(ba.nb + 1) * (kl + ku + 1) * (size_t)h->num_sms * 2048));
+    ba.gb = h->gbuf.as<double2>();
+  }
+  ba.gb_T = gridC * 128;
   CK(cudaEventRecord(h->ev[0], st));
   kp.b<<<(unsigned)gridC, 128, 0, st>>>(ba);
   CK(cudaGetLastError());
@@ -414,23 +438,33 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   // ---- engine B (bisection) on the caller's stream, sharing the SMs with engine L
   if (nB > 0) {
     // Engine B fills what engine L leaves of each SM's register file (L: one 4-warp block per SM).
-    const int tpbB = h->k_btpb;
-    int occM = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, kp.bm, tpbB, 0));
-    occM = std::max(occM, 1);
-    int occShare = occM;
-    if (nA > 0) {
-      cudaFuncAttributes fb, fl;
-      CK(cudaFuncGetAttributes(&fb, kp.bm));
-      CK(cudaFuncGetAttributes(&fl, kp.l));
-      auto warp_regs = [](int r) { return (r * 32 + 255) / 256 * 256; };
-      const int regsL = warp_regs(fl.numRegs) * (int)(gridL > 0 ? kLWarpsPerBlock : 0);
-      const int regsB = warp_regs(fb.numRegs) * (tpbB / 32);
-      occShare = std::max(1, std::min(occM, (65536 - regsL) / regsB));
+    // The block size is the one that fits the most threads there (points rarely outnumber threads by
+    // much, so a second pass over a few leftover points would double the kernel). Launch shape never
+    // changes a result: every sigma is a function of (A, z) only.
+    cudaFuncAttributes fb, fl;
+    CK(cudaFuncGetAttributes(&fb, kp.bm));
+    if (nA > 0) CK(cudaFuncGetAttributes(&fl, kp.l));
+    auto warp_regs = [](int r) { return (r * 32 + 255) / 256 * 256; };
+    int tpbB = 128, occShare = 1;
+    int64_t best = -1;
+    for (int cand : {128, 64, 32}) {
+      if (h->k_btpb > 0 && cand != h->k_btpb) continue;
+      int occM = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, kp.bm, cand, 0));
+      occM = std::max(occM, 1);
+      int occ = occM;
+      if (nA > 0) {
+        const int regsL = warp_regs(fl.numRegs) * (int)(gridL > 0 ? kLWarpsPerBlock : 0);
+        const int regsB = warp_regs(fb.numRegs) * (cand / 32);
+        occ = std::max(1, std::min(occM, (65536 - regsL) / regsB));
+      }
+      const int64_t thr = (int64_t)occ * cand;
+      if (thr > best) { best = thr; tpbB = cand; occShare = occ; }
     }
     gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, (nB * kp.g + tpbB - 1) / tpbB));
     ba.mode = 1;
     ba.max_tests = 200;
+    ba.gb_T = gridB * tpbB;
     kp.bm<<<(unsigned)gridB, tpbB, 0, st>>>(ba);
     CK(cudaGetLastError());
   } else {

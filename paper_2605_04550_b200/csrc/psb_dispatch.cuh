@@ -12,9 +12,10 @@ namespace psb {
 typedef void (*bis_fn)(BisArgs);
 typedef void (*lan_fn)(LanArgs);
 // b: classification (NP = 1); bm: multisection (NP probes per thread); l: Lanczos engine.
+// bt / bmt: the same for bands with a diagonal-constant interior (TZ row loop).
 // (NP probes per lane) x (G lanes per point) are fixed per band shape: results must not depend on
 // the batch. lsmem: Lanczos ring bytes per warp. kl = -1 marks the runtime-shape set.
-struct KPair { int kl, ku; bis_fn b; bis_fn bm; lan_fn l; int lsmem; int np, g; };
+struct KPair { int kl, ku; bis_fn b, bm, bt, bmt; lan_fn l; int lsmem; int np, g; };
 
 void register_shape(const KPair& k);  // defined in psb_capi.cu
 

@@ -13,11 +13,13 @@ namespace psb {
 struct BisArgs {
   int n, kl, ku;
   const double2* __restrict__ Ab;
-  const double2* __restrict__ AHA;
   const double2* __restrict__ zs;
   const int64_t* __restrict__ outidx;  // nullable: output index of point p
   int64_t P;
-  double anorm, tau, rtol;
+  double tau, rtol;
+  const double* __restrict__ offmin;  // min(off-diagonal column, row norm^2) per index j (upper bound)
+  double2 dc;                     // engine-split scale T(z)^2 = (|z - dc| + dr)^2 + offsq >= max_j ||M e_j||^2
+  double dr, offsq;               //   (dc, dr: disc holding A's diagonal; offsq: max off-diagonal column norm^2)
   int force, max_tests;
   double* out;
   int32_t* iters;
@@ -28,6 +30,10 @@ struct BisArgs {
   int mode;                       // 0: classify (one test, split into listA/listB); 1: bisect listB
   int secant;                     // 1: secant-accelerated multisection (G == 1, NP == 2 shapes)
   int tz_j0, tz_j1;               // rows [tz_j0, tz_j1] share one G row (diagonal-constant band); j0 > j1: none
+  double2* gb;                    // TZ kernels: per-thread G rows formed once per point, lane-interleaved
+                                  //   (stride gb_T threads): slots [0, nb) the boundary rows, slot nb the interior row
+  int nb;
+  int64_t gb_T;
   double2* dyn_L;                 // DYN only: per-thread b*b ring
   double* dyn_D;                  // DYN only: per-thread 2b
 };
@@ -322,7 +328,9 @@ __device__ __forceinline__ int64_t out_index(const int64_t* outidx, int64_t p) {
 //   The group keeps [max PD probe, min non-PD probe] (shuffle reductions), so the bracket shrinks
 //   (K+1)-fold per round. (G, NP) depend only on the band shape, never on the batch, so every sigma
 //   is a pure function of (A, z).
-template <int KL, int KU, bool DYN, int NP, int G>
+// TZ: the band has a diagonal-constant interior (a.tz_j0 <= a.tz_j1) whose G row is formed once per
+// round; the general-band row loop is a separate instantiation so each gets its own register budget.
+template <int KL, int KU, bool DYN, int NP, int G, bool TZ>
 __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   constexpr int B = KL + KU;
   constexpr int K = NP * G;
@@ -357,8 +365,10 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           const bool forced = entry < 0;          // forced bisection of a point that failed classification
           const int64_t pt = forced ? ~entry : entry;
           z = a.zs[pt];
-          const double t = a.tau * (hypot(z.x, z.y) + a.anorm);
-          const double lam_tau = t * t;
+          // split at sigma = tau T(z): engine B's squared-form error is c eps T^2 / (2 sigma^2) relative
+          // (c <= 0.6 measured), so sigma >= tau T keeps it below ~1e-10
+          const double dz = hypot(z.x - a.dc.x, z.y - a.dc.y) + a.dr;
+          const double lam_tau = a.tau * a.tau * (dz * dz + a.offsq);
           if (a.mode == 0 && a.force == 1) {  // Lanczos-only mode: hand over immediately
             if (gl == 0) {
               unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
@@ -367,7 +377,30 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           } else {
             p = pt;
             rounds = 0;
+            if constexpr (TZ && !DYN) {
+              // G rows of this point that are not the shared interior row: rows [0, tz_j0) and
+              // (tz_j1, n), then the interior row itself. They depend on z only, so every test of the
+              // point reads them instead of re-forming them (keeps the row loops' registers low).
+              constexpr int B = KL + KU;
+              for (int sl = 0; sl <= a.nb; sl++) {
+                const int i = (sl == a.nb) ? a.tz_j0 : (sl < a.tz_j0 ? sl : a.tz_j1 + 1 + (sl - a.tz_j0));
+#pragma unroll
+                for (int d = 0; d <= B; d++)
+                  a.gb[((int64_t)sl * (B + 1) + d) * a.gb_T + tid] = (i - d >= 0) ? g_entry<KL, KU>(a.n, i, d, a.Ab, z) : czero();
+              }
+            }
             lo = lam_tau; hi = INFINITY; phase = 1;
+            if (a.mode == 1 && !forced) {
+              // upper bound sigma_min^2 <= min_j min(||M e_j||^2, ||e_j^T M||^2): the search then
+              // closes the bracket geometrically from both ends (far points no longer climb from lo)
+              double u2 = INFINITY;
+              for (int j = 0; j < a.n; j++) {
+                const double2 m = csub(z, a.Ab[(int64_t)a.kl * a.n + j]);
+                u2 = fmin(u2, cnorm2(m) + a.offmin[j]);
+              }
+              u2 *= 1.0 + 1e-12;
+              if (u2 > lo) hi = u2;
+            }
             have_lo = have_p = use_sec = false;
             if (a.mode == 1 && forced) { lo = 0.0; hi = lam_tau; phase = 2; }
           }
@@ -386,7 +419,8 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
     for (int q = 0; q < NP; q++) {
       const int i = gl * NP + q;
       if (a.mode == 0) lam[q] = lo;
-      else if (phase == 1) lam[q] = lo * exp2(2.0 * (i + 1));
+      else if (phase == 1) lam[q] = (hi == INFINITY) ? lo * exp2(2.0 * (i + 1))
+                                                      : lo * exp2(log2(hi / lo) * (double)(i + 1) / (double)(K + 1));
       else lam[q] = lo + (hi - lo) * (double)(i + 1) / (double)(K + 1);
       if (!me) lam[q] = 1.0;
     }
@@ -418,20 +452,43 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       LV Ls{a.dyn_L + tid * (int64_t)(b * b > 0 ? b * b : 1), 1};
 #pragma unroll
       for (int q = 0; q < NP; q++)
-        pd[q] = pd_test_dyn(a.n, a.kl, a.ku, a.Ab, a.AHA, zt, lam[q], Ls,
+        pd[q] = pd_test_dyn(a.n, a.kl, a.ku, a.Ab, zt, lam[q], Ls,
                             a.dyn_D + tid * (int64_t)(2 * (b > 0 ? b : 1)), 1);
     } else {
       PDWin<KL, KU> Wn[NP];
       double zz[NP];
 #pragma unroll
-      for (int q = 0; q < NP; q++) zz[q] = cnorm2(zt) - lam[q];
+      for (int q = 0; q < NP; q++) zz[q] = -lam[q];
       // interior rows of a diagonal-constant band: the G row is a function of z only
       double2 gc[B + 1];
-      const bool tz = a.tz_j0 <= a.tz_j1;
+      constexpr bool tz = TZ;
+      // TZ: G row i from the per-point slots (identity padding past n), see the point start
+      auto gslot = [&](int r, int i) {
+        double2 g[B + 1];
+        const int sl = (i < a.tz_j0) ? i : (i <= a.tz_j1 ? a.nb : a.tz_j0 + (i - a.tz_j1 - 1));
 #pragma unroll
-      for (int d = 0; d <= B; d++) gc[d] = tz ? g_entry<KL, KU>(a.n, a.tz_j0, d, a.Ab, a.AHA, zt, 0.0) : czero();
+        for (int d = 0; d <= B; d++)
+          g[d] = (i < a.n && me) ? a.gb[((int64_t)sl * (B + 1) + d) * a.gb_T + tid] : czero();
 #pragma unroll
-      for (int r = 0; r <= B; r++) pdw_load_row<KL, KU, NP>(Wn, r, a.n, r, a.Ab, a.AHA, zt, zz);
+        for (int q = 0; q < NP; q++) {
+#pragma unroll
+          for (int c = 0; c <= B; c++)
+            if (c <= r) Wn[q].W[r][c] = g[r - c];
+          Wn[q].W[r][r].x += (i < a.n) ? zz[q] : 1.0;
+          Wn[q].W[r][r].y = 0.0;
+        }
+      };
+      if constexpr (TZ) {
+#pragma unroll
+        for (int d = 0; d <= B; d++) gc[d] = me ? a.gb[((int64_t)a.nb * (B + 1) + d) * a.gb_T + tid] : czero();
+#pragma unroll
+        for (int r = 0; r <= B; r++) gslot(r, r);
+      } else {
+#pragma unroll
+        for (int d = 0; d <= B; d++) gc[d] = czero();
+#pragma unroll
+        for (int r = 0; r <= B; r++) pdw_load_row<KL, KU, NP>(Wn, r, a.n, r, a.Ab, zt, zz);
+      }
       // Rows run in three segments so no row carries a loader branch: step j loads matrix row
       // j+1+B, which lies in the diagonal-constant interior [tz_j0, tz_j1] for j in [J0, J1).
       // Inside a segment, 8-row blocks are straight-line code (the window shift is register
@@ -477,17 +534,17 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       auto run1 = [&](int j0, int j1) {
         for (int j = j0; j < j1; j++) {
           pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
-          pdw_load_row<KL, KU, NP>(Wn, B, a.n, j + 1 + B, a.Ab, a.AHA, zt, zz);
+          gslot(B, j + 1 + B);
           if (((j - j0) & 7) == 7) norm();
         }
         norm();
       };
-      if (tz) {
+      if constexpr (TZ) {
         run1(0, J0);
         run8(J0, J1, [&](int) { pdw_load_row_g<KL, KU, NP>(Wn, B, gc, zz); });
         if (!stop) run1(J1, a.n);
       } else {
-        run8(0, a.n, [&](int i) { pdw_load_row<KL, KU, NP>(Wn, B, a.n, i, a.Ab, a.AHA, zt, zz); });
+        run8(0, a.n, [&](int i) { pdw_load_row<KL, KU, NP>(Wn, B, a.n, i, a.Ab, zt, zz); });
       }
     }
     if (a.mode == 0) {
@@ -540,8 +597,12 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         const double new_w = nhi - lo;
         use_sec = (phase == 2 || phi < INFINITY) && !(new_w > old_w / 3.0);  // keep going while it pays
       }
-      if (phase == 1 && phi == INFINITY) {
-        lo = nlo;  // every probe PD: keep searching upward
+      if (phase == 1 && nlo < nhi) {
+        // search: upward by 4x/16x while no upper bound, else geometric; the linear multisection /
+        // secant phase starts once the bracket is within a factor 16
+        lo = nlo;
+        hi = nhi;
+        if (hi <= 16.0 * lo) phase = 2;
       } else {
         phase = 2;
         if (nlo >= nhi) {

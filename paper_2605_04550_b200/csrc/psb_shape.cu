@@ -7,12 +7,15 @@ namespace psb {
 namespace {
 
 #ifdef PSB_DYN
-const KPair kSet = {-1, -1, &k_bisect<16, 16, true, 1, 1>, &k_bisect<16, 16, true, 1, 1>,
+const KPair kSet = {-1, -1, &k_bisect<16, 16, true, 1, 1, false>, &k_bisect<16, 16, true, 1, 1, false>,
+                    &k_bisect<16, 16, true, 1, 1, false>, &k_bisect<16, 16, true, 1, 1, false>,
                     &k_lanczos<16, 16, true, 2>, 0, 1, 1};
 #else
 constexpr int D = RingDepth<PSB_KL, PSB_KU>::D;
-const KPair kSet = {PSB_KL, PSB_KU, &k_bisect<PSB_KL, PSB_KU, false, 1, 1>,
-                    &k_bisect<PSB_KL, PSB_KU, false, PSB_NP, PSB_G>, &k_lanczos<PSB_KL, PSB_KU, false, D>,
+const KPair kSet = {PSB_KL, PSB_KU, &k_bisect<PSB_KL, PSB_KU, false, 1, 1, false>,
+                    &k_bisect<PSB_KL, PSB_KU, false, PSB_NP, PSB_G, false>,
+                    &k_bisect<PSB_KL, PSB_KU, false, 1, 1, true>,
+                    &k_bisect<PSB_KL, PSB_KU, false, PSB_NP, PSB_G, true>, &k_lanczos<PSB_KL, PSB_KU, false, D>,
                     Ring<PSB_KL, PSB_KU, D>::BYTES, PSB_NP, PSB_G};
 #endif
 

@@ -1,5 +1,5 @@
 """Full-grid error of the bisection engine near the classification threshold: for every point that
-moves from engine L (tau=3e-3) to engine B at a lower tau, compare the two results. Engine L is
+moves from engine L (tau=1e-2) to engine B at a lower tau, compare the two results. Engine L is
 accurate there (C1-C4 fixtures: <= 1e-11), so this measures engine B's squared-form error as a
 function of r = sigma/S over whole grids, with c = err * 2 r^2 / eps the empirical rounding
 constant (development tool)."""
@@ -13,10 +13,14 @@ cfg = configs.CONFIGS[name]
 A = cfg.matrix()
 pts = cfg.grid.points().ravel()
 h = _lib.handle()
-ref, it0, st0 = core.smin_many(A, pts, opts=_lib.make_opts(tau=3e-3), return_info=True)
+TAU_REF = 1e-2
+ref, it0, st0 = core.smin_many(A, pts, opts=_lib.make_opts(tau=TAU_REF), return_info=True)
 Ad = A.todense()
-an = np.sqrt(np.abs(Ad).sum(0).max() * np.abs(Ad).sum(1).max())
-S = np.abs(pts) + an
+dg = np.diag(Ad)
+c0 = 0.5 * (dg.real.min() + dg.real.max()) + 0.5j * (dg.imag.min() + dg.imag.max())
+r0 = np.abs(dg - c0).max()
+offsq = (np.abs(Ad - np.diag(dg)) ** 2).sum(0).max()
+S = np.sqrt((np.abs(pts - c0) + r0) ** 2 + offsq)  # the engine split's scale T(z)
 for tau in taus:
     v, it, st = core.smin_many(A, pts, opts=_lib.make_opts(tau=tau), return_info=True)
     moved = np.flatnonzero((st0 == 0) & (st == 1))
