@@ -476,6 +476,19 @@ PSB_HD double2 g_entry(int n, int j, int d, const double2* __restrict__ Ab, doub
   return v;
 }
 
+// The same entry from the expansion G = A^H A - conj(z) A - z A^H + |z|^2 I (AHA[d * n + j] =
+// (A^H A)[j, j-d], precomputed per matrix; the |z|^2 - lam diagonal term is the caller's zz). Three
+// terms per entry instead of b - d + 1 products, with rounding relative to (|z| + ||A||)^2: the form
+// of the general-band kernels, whose engine split uses that scale.
+template <int KLM, int KUM>
+PSB_HD double2 g_entry_aha(int n, int j, int d, const double2* __restrict__ Ab, const double2* __restrict__ AHA,
+                           double2 z) {
+  double2 v = AHA[(int64_t)d * n + j];
+  if (d <= KLM) v = cfms_cj(v, z, Ab[(int64_t)(KLM - d) * n + j]);             // - conj(z) A[j, j-d]
+  if (d <= KUM) v = cfms(v, z, cconj(Ab[(int64_t)(KLM + d) * n + (j - d)]));  // - z conj(A[j-d, j])
+  return v;
+}
+
 // One row of the factorization for static shapes, for NP independent shifts lambda_q that share
 // the off-diagonal G entries (only the diagonal depends on lambda). U = j mod B (compile-time).
 template <int KLM, int KUM, int NP, int U>
@@ -535,16 +548,17 @@ struct PDWin {
   double2 W[B + 1][B + 1];
 };
 
-template <int KLM, int KUM, int NP>
+template <int KLM, int KUM, int NP, bool AHAF = false>
 PSB_HD void pdw_load_row(PDWin<KLM, KUM> (&Wn)[NP], int r, int n, int i, const double2* __restrict__ Ab,
-                         double2 z, const double (&zz)[NP]) {
+                         double2 z, const double (&zz)[NP], const double2* __restrict__ AHA = nullptr) {
   // row r of the window = matrix row i, columns i-r .. i (G entries G[i, i-d], d = r - c)
   constexpr int B = KLM + KUM;
   double2 g[B + 1];
 #pragma unroll
   for (int d = 0; d <= B; d++) {
     g[d] = czero();
-    if (d <= r && i < n && i - d >= 0) g[d] = g_entry<KLM, KUM>(n, i, d, Ab, z);
+    if (d <= r && i < n && i - d >= 0)
+      g[d] = AHAF ? g_entry_aha<KLM, KUM>(n, i, d, Ab, AHA, z) : g_entry<KLM, KUM>(n, i, d, Ab, z);
   }
 #pragma unroll
   for (int q = 0; q < NP; q++) {
@@ -672,23 +686,18 @@ PSB_HD bool pd_test_static(int n, const double2* __restrict__ Ab, double2 z,
 }
 
 // Runtime-shape PD test (any kl, ku; ring in a caller-provided scratch of b*b complex + 2b doubles).
-PSB_HD bool pd_test_dyn(int n, int kl, int ku, const double2* __restrict__ Ab,
+// (general-band form: G from the A^H A expansion, see g_entry_aha)
+PSB_HD bool pd_test_dyn(int n, int kl, int ku, const double2* __restrict__ Ab, const double2* __restrict__ AHA,
                         double2 z, double lam, LV Lsc, double* Dsc, int dld) {
   const int b = kl + ku;
-  // G[j, j-d] from M's entries (see g_entry)
-  auto gent = [&](int j, int d) {
-    double2 v = czero();
-    for (int t = 0; t <= b - d; t++) {
-      const int k = j - ku + t;
-      if (k < 0 || k >= n) continue;
-      const double2 m1 = m_entry(Ab, n, kl, k, ku - t, z), m2 = m_entry(Ab, n, kl, k, ku - t - d, z);
-      v = cfms_cj(v, cmk(-m1.x, -m1.y), m2);
-    }
-    return v;
-  };
+  const double zz = cnorm2(z) - lam;
   if (b == 0) {  // diagonal A
-    for (int j = 0; j < n; j++)
-      if (!(gent(j, 0).x - lam > 0.0)) return false;
+    for (int j = 0; j < n; j++) {
+      double2 v = AHA[j];
+      v = cfms_cj(v, z, Ab[j]);
+      v = cfms(v, z, cconj(Ab[j]));
+      if (!(v.x + zz > 0.0)) return false;
+    }
     return true;
   }
   for (int s = 0; s < b; s++) {
@@ -700,14 +709,22 @@ PSB_HD bool pd_test_dyn(int n, int kl, int ku, const double2* __restrict__ Ab,
   for (int j = 0; j < n; j++) {
     for (int d = b; d >= 1; d--) {
       const int c = j - d;
-      const double2 g = (c >= 0) ? gent(j, d) : czero();
+      double2 g = czero();
+      if (c >= 0) {
+        g = AHA[(int64_t)d * n + j];
+        if (d <= kl) g = cfms_cj(g, z, Ab[(int64_t)(kl - d) * n + j]);
+        if (d <= ku) g = cfms(g, z, cconj(Ab[(int64_t)(kl + d) * n + c]));
+      }
       const int sc = ((c % b) + b) % b;
       double2 sacc = g;
       for (int dm = b; dm > d; dm--) sacc = cfms_cj(sacc, Lsc.get((int64_t)sc * b + dm - d - 1), LD[dm]);
       Lj[d] = cscale(sacc, Dsc[(int64_t)(2 * sc + 1) * dld]);
       LD[d] = cscale(Lj[d], Dsc[(int64_t)(2 * sc) * dld]);
     }
-    double dj = gent(j, 0).x - lam;
+    double2 g0 = AHA[j];
+    g0 = cfms_cj(g0, z, Ab[(int64_t)kl * n + j]);
+    g0 = cfms(g0, z, cconj(Ab[(int64_t)kl * n + j]));
+    double dj = g0.x + zz;
     for (int d = 1; d <= b; d++) dj -= cdotr(Lj[d], LD[d]);
     if (!(dj > 0.0)) return false;
     const int s0 = j % b;

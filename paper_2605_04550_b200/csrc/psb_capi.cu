@@ -71,6 +71,7 @@ struct psb_handle {
   int n = 0, kl = 0, ku = 0;
   double2 dc{0.0, 0.0};  // engine-split scale (BisArgs): disc of A's diagonal, max off-diagonal column norm^2
   double dr = 0.0, offsq = 0.0;
+  double anorm = 0.0;    // general-band kernels' split scale: sqrt(||A||_1 ||A||_inf) >= ||A||_2
   int tz_j0 = 1, tz_j1 = 0;  // interior rows sharing one G row (diagonal-constant band), empty by default
   // development knobs, read once at psb_create (A/B switches; defaults are the product path):
   //   PSB_TAU=x default engine split, PSB_BTPB=n engine-B block size, PSB_NOSEC=1 plain multisection, PSB_NOTZ=1 per-row G formation, PSB_LWARPS=N cap on
@@ -80,7 +81,7 @@ struct psb_handle {
   int k_btpb = 128;
   double k_tau = 0.0;
   bool have_matrix = false;
-  DevBuf Ab, v1, offmin, gbuf;
+  DevBuf Ab, AHA, v1, offmin, gbuf;
   // per call
   DevBuf zs, outidx, out, iters, status, listA, listB, counters, scratch, pivs, dynL, dynD;
   DevBuf xs, ys, prof;
@@ -169,7 +170,7 @@ int psb_create(int device, psb_handle** out) {
 void psb_destroy(psb_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  DevBuf* bufs[] = {&h->Ab, &h->v1, &h->offmin, &h->gbuf, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
+  DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->v1, &h->offmin, &h->gbuf, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
                     &h->counters, &h->scratch, &h->pivs, &h->dynL, &h->dynD, &h->xs, &h->ys, &h->params,
                     &h->feat, &h->eig, &h->prob, &h->region, &h->idx};
   for (DevBuf* b : bufs) b->release();
@@ -239,6 +240,34 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
     h->dc = make_double2(c.real(), c.imag());
     h->dr = r * (1.0 + 1e-15);
     h->offsq = *std::max_element(off.begin(), off.end()) * (1.0 + 1e-15);
+  }
+  // General-band kernels: A^H A band AHA[d*n + j] = (A^H A)[j, j-d] = sum_k conj(A[k, j]) A[k, j-d], and
+  // ||A||_2 <= sqrt(||A||_1 ||A||_inf) for their split scale
+  {
+    auto Aat = [&](int i, int c) -> cd {
+      const int d = c - i;
+      if (d < -kl || d > ku || i < 0 || c < 0 || i >= n || c >= n) return cd(0, 0);
+      return A[(int64_t)(d + kl) * n + i];
+    };
+    std::vector<cd> aha((size_t)(b + 1) * n, cd(0, 0));
+    for (int j = 0; j < n; j++)
+      for (int d = 0; d <= b && j - d >= 0; d++) {
+        const int c = j - d;
+        cd acc(0, 0);
+        for (int k = std::max(0, j - ku); k <= std::min(n - 1, c + kl); k++) acc += std::conj(Aat(k, j)) * Aat(k, c);
+        aha[(size_t)d * n + j] = acc;
+      }
+    std::vector<double> colsum(n, 0.0), rowsum(n, 0.0);
+    for (int d = -kl; d <= ku; d++)
+      for (int i = 0; i < n; i++) {
+        if (i + d < 0 || i + d >= n) continue;
+        const double m = std::abs(A[(int64_t)(d + kl) * n + i]);
+        rowsum[i] += m;
+        colsum[i + d] += m;
+      }
+    h->anorm = std::sqrt(*std::max_element(colsum.begin(), colsum.end()) * *std::max_element(rowsum.begin(), rowsum.end()));
+    CK(h->AHA.ensure(sizeof(cd) * (b + 1) * n));
+    CK(cudaMemcpy(h->AHA.p, aha.data(), sizeof(cd) * (b + 1) * n, cudaMemcpyHostToDevice));
   }
   // Lanczos start vector: fixed, identical for every z (determinism)
   std::vector<cd> v1(n);
@@ -347,9 +376,9 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   occB = std::max(occB, 1);
   BisArgs ba;
   ba.n = n; ba.kl = kl; ba.ku = ku;
-  ba.Ab = h->Ab.as<double2>(); ba.offmin = h->offmin.as<double>();
+  ba.Ab = h->Ab.as<double2>(); ba.AHA = h->AHA.as<double2>(); ba.offmin = h->offmin.as<double>();
   ba.zs = d_zs; ba.outidx = d_outidx; ba.P = P;
-  ba.dc = h->dc; ba.dr = h->dr; ba.offsq = h->offsq; ba.tau = opt.tau; ba.rtol = opt.bis_rtol;
+  ba.anorm = h->anorm; ba.dc = h->dc; ba.dr = h->dr; ba.offsq = h->offsq; ba.tau = opt.tau; ba.rtol = opt.bis_rtol;
   ba.force = opt.force_engine; ba.max_tests = 400;
   ba.out = d_out; ba.iters = d_iters; ba.status = d_status;
   ba.listA = h->listA.as<int64_t>(); ba.listB = h->listB.as<int64_t>(); ba.counters = cnt;

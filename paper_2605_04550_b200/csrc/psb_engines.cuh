@@ -13,12 +13,14 @@ namespace psb {
 struct BisArgs {
   int n, kl, ku;
   const double2* __restrict__ Ab;
+  const double2* __restrict__ AHA;  // (A^H A)[j, j-d] band: G rows of the general-band kernels
   const double2* __restrict__ zs;
   const int64_t* __restrict__ outidx;  // nullable: output index of point p
   int64_t P;
   double tau, rtol;
   const double* __restrict__ offmin;  // min(off-diagonal column, row norm^2) per index j (upper bound)
-  double2 dc;                     // engine-split scale T(z)^2 = (|z - dc| + dr)^2 + offsq >= max_j ||M e_j||^2
+  double anorm;                   // general-band kernels: split scale S(z) = |z| + sqrt(||A||_1 ||A||_inf)
+  double2 dc;                     // TZ kernels: engine-split scale T(z)^2 = (|z - dc| + dr)^2 + offsq >= max_j ||M e_j||^2
   double dr, offsq;               //   (dc, dr: disc holding A's diagonal; offsq: max off-diagonal column norm^2)
   int force, max_tests;
   double* out;
@@ -367,8 +369,14 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           z = a.zs[pt];
           // split at sigma = tau T(z): engine B's squared-form error is c eps T^2 / (2 sigma^2) relative
           // (c <= 0.6 measured), so sigma >= tau T keeps it below ~1e-10
-          const double dz = hypot(z.x - a.dc.x, z.y - a.dc.y) + a.dr;
-          const double lam_tau = a.tau * a.tau * (dz * dz + a.offsq);
+          double lam_tau;
+          if constexpr (TZ && !DYN) {  // G formed from M's entries: rounding relative to T(z)^2
+            const double dz = hypot(z.x - a.dc.x, z.y - a.dc.y) + a.dr;
+            lam_tau = a.tau * a.tau * (dz * dz + a.offsq);
+          } else {  // G from the A^H A expansion: rounding relative to S(z)^2 = (|z| + ||A||)^2
+            const double sz = hypot(z.x, z.y) + a.anorm;
+            lam_tau = a.tau * a.tau * sz * sz;
+          }
           if (a.mode == 0 && a.force == 1) {  // Lanczos-only mode: hand over immediately
             if (gl == 0) {
               unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
@@ -452,13 +460,13 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       LV Ls{a.dyn_L + tid * (int64_t)(b * b > 0 ? b * b : 1), 1};
 #pragma unroll
       for (int q = 0; q < NP; q++)
-        pd[q] = pd_test_dyn(a.n, a.kl, a.ku, a.Ab, zt, lam[q], Ls,
+        pd[q] = pd_test_dyn(a.n, a.kl, a.ku, a.Ab, a.AHA, zt, lam[q], Ls,
                             a.dyn_D + tid * (int64_t)(2 * (b > 0 ? b : 1)), 1);
     } else {
       PDWin<KL, KU> Wn[NP];
       double zz[NP];
 #pragma unroll
-      for (int q = 0; q < NP; q++) zz[q] = -lam[q];
+      for (int q = 0; q < NP; q++) zz[q] = TZ ? -lam[q] : cnorm2(zt) - lam[q];  // (see g_entry_aha)
       // interior rows of a diagonal-constant band: the G row is a function of z only
       double2 gc[B + 1];
       constexpr bool tz = TZ;
@@ -487,7 +495,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
 #pragma unroll
         for (int d = 0; d <= B; d++) gc[d] = czero();
 #pragma unroll
-        for (int r = 0; r <= B; r++) pdw_load_row<KL, KU, NP>(Wn, r, a.n, r, a.Ab, zt, zz);
+        for (int r = 0; r <= B; r++) pdw_load_row<KL, KU, NP, true>(Wn, r, a.n, r, a.Ab, zt, zz, a.AHA);
       }
       // Rows run in three segments so no row carries a loader branch: step j loads matrix row
       // j+1+B, which lies in the diagonal-constant interior [tz_j0, tz_j1] for j in [J0, J1).
@@ -544,7 +552,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         run8(J0, J1, [&](int) { pdw_load_row_g<KL, KU, NP>(Wn, B, gc, zz); });
         if (!stop) run1(J1, a.n);
       } else {
-        run8(0, a.n, [&](int i) { pdw_load_row<KL, KU, NP>(Wn, B, a.n, i, a.Ab, zt, zz); });
+        run8(0, a.n, [&](int i) { pdw_load_row<KL, KU, NP, true>(Wn, B, a.n, i, a.Ab, zt, zz, a.AHA); });
       }
     }
     if (a.mode == 0) {

@@ -15,6 +15,7 @@ RAW = ['dram__bytes_read.sum', 'dram__bytes_write.sum', 'sm__pipe_fp64_cycles_ac
 def details(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
+    r = r[next(i for i, row in enumerate(r) if 'Kernel Name' in row):]
     h = r[0]
     ki, ii, mi, vi, ui = (h.index('Kernel Name'), h.index('ID'), h.index('Metric Name'), h.index('Metric Value'),
                           h.index('Metric Unit'))
@@ -28,6 +29,7 @@ def details(rep):
 def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(out.splitlines()))
+    r = r[next(i for i, row in enumerate(r) if 'Kernel Name' in row):]
     h, units, rows = r[0], r[1], r[2:]
     res = {}
     stall = {}
