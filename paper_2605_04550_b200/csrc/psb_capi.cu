@@ -74,12 +74,13 @@ struct psb_handle {
   double anorm = 0.0;    // general-band kernels' split scale: sqrt(||A||_1 ||A||_inf) >= ||A||_2
   int tz_j0 = 1, tz_j1 = 0;  // interior rows sharing one G row (diagonal-constant band), empty by default
   // development knobs, read once at psb_create (A/B switches; defaults are the product path):
-  //   PSB_TAU=x default engine split, PSB_BTPB=n engine-B block size, PSB_NOSEC=1 plain multisection, PSB_NOTZ=1 per-row G formation, PSB_LWARPS=N cap on
+  //   PSB_TAU=x default engine split, PSB_NOBEXP=1 no second engine-B launch, PSB_BTPB=n engine-B block size, PSB_NOSEC=1 plain multisection, PSB_NOTZ=1 per-row G formation, PSB_LWARPS=N cap on
   //   Lanczos warps, PSB_PROF=1 per-phase clock64 counters of the Lanczos kernel (stderr)
   bool k_secant = true, k_toeplitz = true, k_prof = false;
   long long k_lwarps = 0;
   int k_btpb = 128;
   double k_tau = 0.0;
+  bool k_bexpand = true;
   bool have_matrix = false;
   DevBuf Ab, AHA, v1, offmin, gbuf;
   // per call
@@ -157,6 +158,7 @@ int psb_create(int device, psb_handle** out) {
   h->k_secant = getenv("PSB_NOSEC") == nullptr;
   h->k_toeplitz = getenv("PSB_NOTZ") == nullptr;
   h->k_prof = getenv("PSB_PROF") != nullptr;
+  h->k_bexpand = getenv("PSB_NOBEXP") == nullptr;
   h->k_tau = getenv("PSB_TAU") ? atof(getenv("PSB_TAU")) : 0.0;  // dev: default engine split
   h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 0;  // 0: pick per launch
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
@@ -388,7 +390,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.tz_j0 = h->k_toeplitz ? h->tz_j0 : 1;
   ba.tz_j1 = h->k_toeplitz ? h->tz_j1 : 0;
   const int64_t gridC = std::max<int64_t>(1, std::min<int64_t>((int64_t)occB * h->num_sms, (P + 127) / 128));
-  int64_t gridB = (int64_t)occB * h->num_sms;
+  int64_t gridB = (int64_t)occB * h->num_sms, gridB2 = 0;
   if (dyn) {
     const int b = std::max(kl + ku, 1);
     const int64_t threads = std::max(gridB, gridC) * 128;
@@ -396,7 +398,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     CK(h->dynD.ensure(sizeof(double) * threads * 2 * b));
     ba.dyn_L = h->dynL.as<double2>(); ba.dyn_D = h->dynD.as<double>();
   }
-  ba.gb = nullptr; ba.nb = 0; ba.gb_T = 0;
+  ba.gb = nullptr; ba.nb = 0; ba.gb_T = 0; ba.tid_base = 0;
   const bool tzk = !dyn && h->tz_j0 <= h->tz_j1 && h->k_toeplitz;
   if (tzk) {
     // per-thread G-row slots of the TZ kernels; any persistent grid has <= 2048 threads per SM
@@ -474,7 +476,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     CK(cudaFuncGetAttributes(&fb, kp.bm));
     if (nA > 0) CK(cudaFuncGetAttributes(&fl, kp.l));
     auto warp_regs = [](int r) { return (r * 32 + 255) / 256 * 256; };
-    int tpbB = 128, occShare = 1;
+    int tpbB = 128, occShare = 1, occFull = 1;
     int64_t best = -1;
     for (int cand : {128, 64, 32}) {
       if (h->k_btpb > 0 && cand != h->k_btpb) continue;
@@ -488,19 +490,43 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
         occ = std::max(1, std::min(occM, (65536 - regsL) / regsB));
       }
       const int64_t thr = (int64_t)occ * cand;
-      if (thr > best) { best = thr; tpbB = cand; occShare = occ; }
+      if (thr > best) { best = thr; tpbB = cand; occShare = occ; occFull = occM; }
     }
-    gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, (nB * kp.g + tpbB - 1) / tpbB));
+    const int64_t wantB = (nB * kp.g + tpbB - 1) / tpbB;
+    gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, wantB));
+    // A second launch, queued behind engine L on its stream, takes the SM share engine L releases when
+    // it finishes (both launches pull from the same work counter), so a long bisection tail runs at
+    // full occupancy instead of the share it had next to engine L.
+    // Only for long lists (>= 4 points per thread after the expansion): with ~1-2 points per thread the
+    // late starters' last points stretch the tail by a point's latency (C3: +4%; C5: -15%).
+    if (nA > 0 && gridL > 0 && h->k_bexpand) {
+      const int64_t extra = std::max<int64_t>(0, std::min<int64_t>((int64_t)occFull * h->num_sms, wantB) - gridB);
+      if (nB * kp.g >= 4 * (gridB + extra) * tpbB) gridB2 = extra;
+    }
     ba.mode = 1;
     ba.max_tests = 200;
-    ba.gb_T = gridB * tpbB;
+    ba.gb_T = (gridB + gridB2) * tpbB;
+    ba.tid_base = 0;
+    if (dyn) {
+      CK(h->dynL.ensure(sizeof(double2) * (size_t)ba.gb_T * std::max(kl + ku, 1) * std::max(kl + ku, 1)));
+      CK(h->dynD.ensure(sizeof(double) * (size_t)ba.gb_T * 2 * std::max(kl + ku, 1)));
+      ba.dyn_L = h->dynL.as<double2>(); ba.dyn_D = h->dynD.as<double>();
+    }
     kp.bm<<<(unsigned)gridB, tpbB, 0, st>>>(ba);
     CK(cudaGetLastError());
+    if (gridB2 > 0) {
+      BisArgs b2 = ba;
+      b2.tid_base = gridB * tpbB;
+      kp.bm<<<(unsigned)gridB2, tpbB, 0, h->stream2>>>(b2);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(h->ev[6], h->stream2));
+    }
   } else {
     gridB = 0;
   }
   CK(cudaEventRecord(h->ev[2], st));
   if (nA > 0) CK(cudaStreamWaitEvent(st, h->ev[3], 0));
+  if (gridB2 > 0) CK(cudaStreamWaitEvent(st, h->ev[6], 0));
   CK(cudaEventRecord(h->ev[4], st));
   unsigned long long hc[8];
   CK(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
@@ -509,6 +535,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   float msC = 0, msB = 0, msL = 0, msT = 0;
   cudaEventElapsedTime(&msC, h->ev[0], h->ev[1]);
   cudaEventElapsedTime(&msB, h->ev[1], h->ev[2]);
+  if (gridB2 > 0) { float m2 = 0; cudaEventElapsedTime(&m2, h->ev[1], h->ev[6]); msB = std::max(msB, m2); }
   if (nA > 0) cudaEventElapsedTime(&msL, h->ev[1], h->ev[3]);
   cudaEventElapsedTime(&msT, h->ev[0], h->ev[4]);
   if (h->k_prof && nA_run > 0) {

@@ -36,6 +36,7 @@ struct BisArgs {
                                   //   (stride gb_T threads): slots [0, nb) the boundary rows, slot nb the interior row
   int nb;
   int64_t gb_T;
+  int64_t tid_base;               // first thread index of this launch (engine B runs as one or two launches)
   double2* dyn_L;                 // DYN only: per-thread b*b ring
   double* dyn_D;                  // DYN only: per-thread 2b
 };
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;               // lane within the group
   const int leader = lane - gl;          // group leader lane
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tid = a.tid_base + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t p = -1;
   double2 z = czero();
   double lo = 0.0, hi = 0.0;
