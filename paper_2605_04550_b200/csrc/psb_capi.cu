@@ -560,7 +560,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   S.flops_lanczos = (double)hc[6] * n * flops_lu_row(kl, ku) + (double)hc[5] * n * flops_it_row(kl, ku);
   S.bytes_lanczos = (double)hc[6] * n * (16.0 * (s.NU + kl) + 4.0) + (double)hc[5] * n * bytes_it_row(kl, ku);
   S.ms_bisect = msC + msB; S.ms_lanczos = msL; S.ms_total = msT;
-  S.grid_bisect = (int32_t)gridB; S.grid_lanczos = (int32_t)gridL;
+  S.grid_bisect = (int32_t)(gridB + gridB2); S.grid_lanczos = (int32_t)gridL;
   if ((int64_t)(hc[3] + hc[6]) != P)
     return fail(h, PSB_ERR_CUDA, "internal: points finished " + std::to_string(hc[3] + hc[6]) + " != " +
                                      std::to_string(P));

@@ -202,3 +202,23 @@ def test_bisection_near_threshold_full_grid(gpu, name):
     assert moved.sum() > 100
     e = np.abs(got[moved] - ref[moved]) / ref[moved]
     assert e.max() <= 1e-9, f"{name}: worst {e.max():.3e}"
+
+
+def test_engine_b_second_launch_is_bitwise_neutral(gpu, tmp_path):
+    """Long bisection lists run as two launches (the second queued behind engine L); launch shape must
+    not change a single bit. C5's full 1024x1024 grid (about 300k bisection points) takes that path;
+    PSB_NOBEXP=1 (read at handle creation, so in a subprocess) runs it as one launch."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, '.'); from paper_2605_04550_b200 import configs, core; "
+            "c = configs.CONFIGS['C5']; np.save(sys.argv[1], core.smin_many(c.matrix(0), c.grid.points().ravel()))")
+    outs = []
+    for env_extra, name in (({}, "two.npy"), ({"PSB_NOBEXP": "1"}, "one.npy")):
+        env = {k: v for k, v in os.environ.items() if k != "PSB_NOBEXP"}
+        env.update(env_extra)
+        path = tmp_path / name
+        subprocess.run([sys.executable, "-c", code, str(path)], check=True, env=env,
+                       cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
