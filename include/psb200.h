@@ -47,8 +47,10 @@ extern "C" {
 typedef struct psb_handle psb_handle;
 
 typedef struct {
-  double tau;          /* engine split: sigma >= tau*T(z) -> bisection engine (default 1.5e-3);
-                          T(z)^2 = (|z-c|+r)^2 + max off-diagonal column norm^2 of A bounds zI-A's columns */
+  double tau;          /* engine split: sigma >= tau*X(z) -> bisection engine (default 1.5e-3). X is the
+                          scale the bisection engine's G = (zI-A)^H (zI-A) is rounded at: for bands with a
+                          diagonal-constant interior T(z), T^2 = (|z-c|+r)^2 + max off-diagonal column
+                          norm^2 of A; otherwise S(z) = |z| + sqrt(||A||_1 ||A||_inf) */
   double bis_rtol;     /* bisection stop: (hi-lo) <= bis_rtol*hi on lambda = sigma^2 (default 2e-12) */
   int32_t kmax;        /* Lanczos step cap (0 -> min(3000, max(64, 4n))) */
   int32_t force_engine;/* 0 auto, 1 Lanczos engine only, 2 bisection engine only (testing) */
