@@ -314,7 +314,8 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
       int j0 = m, j1 = m;
       while (j0 - 1 >= b && same_row(j0 - 1, m)) j0--;
       while (j1 + 1 + kl < n && same_row(j1 + 1, m)) j1++;
-      if (j1 - j0 >= 16) { h->tz_j0 = j0; h->tz_j1 = j1; }
+      // the TZ kernels keep a point's boundary G rows in per-thread slots: only for short boundaries
+      if (j1 - j0 >= 16 && j0 + (n - 1 - j1) <= 32) { h->tz_j0 = j0; h->tz_j1 = j1; }
     }
   }
   h->have_matrix = true;
@@ -401,9 +402,9 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.gb = nullptr; ba.nb = 0; ba.gb_T = 0; ba.tid_base = 0;
   const bool tzk = !dyn && h->tz_j0 <= h->tz_j1 && h->k_toeplitz;
   if (tzk) {
-    // per-thread G-row slots of the TZ kernels; any persistent grid has <= 2048 threads per SM
+    // per-thread G-row slots of the TZ kernels (boundary rows + the interior row), sized per launch
     ba.nb = h->tz_j0 + (n - 1 - h->tz_j1);
-    CK(h->gbuf.ensure(sizeof(double2) * (size_t)(ba.nb + 1) * (kl + ku + 1) * (size_t)h->num_sms * 2048));
+    CK(h->gbuf.ensure(sizeof(double2) * (size_t)(ba.nb + 1) * (kl + ku + 1) * (size_t)(gridC * 128)));
     ba.gb = h->gbuf.as<double2>();
   }
   ba.gb_T = gridC * 128;
@@ -507,6 +508,10 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     ba.max_tests = 200;
     ba.gb_T = (gridB + gridB2) * tpbB;
     ba.tid_base = 0;
+    if (tzk) {  // after the host round trip the classification kernel is done: resizing is safe
+      CK(h->gbuf.ensure(sizeof(double2) * (size_t)(ba.nb + 1) * (kl + ku + 1) * (size_t)ba.gb_T));
+      ba.gb = h->gbuf.as<double2>();
+    }
     if (dyn) {
       CK(h->dynL.ensure(sizeof(double2) * (size_t)ba.gb_T * std::max(kl + ku, 1) * std::max(kl + ku, 1)));
       CK(h->dynD.ensure(sizeof(double) * (size_t)ba.gb_T * 2 * std::max(kl + ku, 1)));

@@ -222,3 +222,17 @@ def test_engine_b_second_launch_is_bitwise_neutral(gpu, tmp_path):
                        cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_partly_constant_band_long_boundary(gpu):
+    """A band that is diagonal-constant only over its second half: the constant interior is long
+    enough to detect but its boundary (60 rows) exceeds the per-thread slot budget, so the general
+    kernels run. Against the oracle at points on both sides of the engine split."""
+    from oracle.sigma_oracle import smin_restated
+    A = configs.grcar_band(120).todense().real.copy()
+    rng = np.random.default_rng(11)
+    for i in range(60):
+        for j in range(max(0, i - 1), min(120, i + 4)):
+            A[i, j] += 0.3 * rng.standard_normal()
+    zs = np.concatenate([core.make_grid(-1, 3, -3.5, 3.5, 6, 6).points().ravel(), [0.5 + 1.2j, 2.9 + 0.1j]])
+    check(core.smin_many(A, zs), smin_restated(A, zs), np.linalg.norm(A, 2), "partly constant band")
