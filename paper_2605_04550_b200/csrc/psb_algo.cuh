@@ -432,12 +432,16 @@ PSB_HD double ritz_top(const double2* hist, int ld, int k, double theta_prev, do
   return x;
 }
 
-// Convergence rule (measured on C1..C4 against zgesdd):
-// stop when the Ritz residual r = beta_k |s_k| is below 1e-10 theta, or below 1e-6 theta
-// with the Ritz value stationary to 1e-12.
+// Convergence rule: stop when the Ritz residual r = beta_k |s_k| is below 1e-10 theta,
+// or below 1e-8 theta with the Ritz value stationary to 1e-13.
+// The stationary branch bounds the Ritz error by r^2 / gap <= 1e-16 theta^2 / gap, i.e. <= 1e-10 theta
+// for gaps down to 1e-6 theta. (It was r <= 1e-6 theta with dtheta <= 1e-12 theta: a random diagonal
+// band with a 4e-5 relative cluster at sigma_min stopped 8.5e-9 off, found by tools/fuzz_parity.py;
+// the tighter rule costs +0.2..1.6% Lanczos steps on C2-C5.) r <= 1e-10 theta alone is not reachable
+// everywhere: rounding floors the residual of some ill-conditioned shifts above it.
 PSB_HD bool lanczos_converged(double theta, double dtheta, double r, double beta) {
   if (beta == 0.0) return true;
-  return (r <= 1e-6 * theta && dtheta <= 1e-12 * theta) || r <= 1e-10 * theta;
+  return (r <= 1e-8 * theta && dtheta <= 1e-13 * theta) || r <= 1e-10 * theta;
 }
 
 // --------------------------------------------------------- engine B: PD test

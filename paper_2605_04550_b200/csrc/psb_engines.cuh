@@ -30,6 +30,8 @@ struct BisArgs {
   int64_t* listB;                 // points the bisection engine owns (mode 1 input)
   unsigned long long* counters;   // [0] work, [1] nA, [2] pd tests, [3] nB done, [7] nB listed
   int mode;                       // 0: classify (one test, split into listA/listB); 1: bisect listB
+  int fallback;                   // 1: listB holds engine-L points that did not converge (forced, [0, lambda_tau]);
+  double rmin2;                   //    their result is kept only where sigma^2 >= rmin2 X(z)^2 (squared form accurate)
   int secant;                     // 1: secant-accelerated multisection (G == 1, NP == 2 shapes)
   int tz_j0, tz_j1;               // rows [tz_j0, tz_j1] share one G row (diagonal-constant band); j0 > j1: none
   double2* gb;                    // TZ kernels: per-thread G rows formed once per point, lane-interleaved
@@ -49,7 +51,8 @@ struct LanArgs {
   const double2* __restrict__ zs;
   const int64_t* __restrict__ outidx;
   const int64_t* __restrict__ listA;
-  unsigned long long* counters;   // [1] nA (read), [4] work, [5] lanczos steps, [6] nL
+  unsigned long long* counters;   // [1] nA (read), [4] work, [5] lanczos steps, [6] nL, [8] n not converged
+  int64_t* listF;                 // not-converged points (as ~p: forced bisection entries), counters[8] of them
   double* out;
   int32_t* iters;
   int8_t* status;
@@ -347,6 +350,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   double2 z = czero();
   double lo = 0.0, hi = 0.0;
   int phase = 1, rounds = 0;
+  double x2 = 0.0;  // X(z)^2 of the lane's point
   // secant acceleration state (G == 1): log det at lo and at the previous PD point lp
   double Llo = 0.0, lp = 0.0, Lp = 0.0;
   bool have_lo = false, have_p = false, use_sec = false;
@@ -371,7 +375,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           // split at sigma = tau T(z): engine B's squared-form error is c eps T^2 / (2 sigma^2) relative
           // (c <= 0.6 measured), so sigma >= tau T keeps it below ~1e-10
           double lam_tau;
-          if constexpr (TZ && !DYN) {  // G formed from M's entries: rounding relative to T(z)^2
+          if constexpr (TZ && !DYN) {  // (x2 = X(z)^2 = lam_tau / tau^2, kept for the fallback check)  // G formed from M's entries: rounding relative to T(z)^2
             const double dz = hypot(z.x - a.dc.x, z.y - a.dc.y) + a.dr;
             lam_tau = a.tau * a.tau * (dz * dz + a.offsq);
           } else {  // G from the A^H A expansion: rounding relative to S(z)^2 = (|z| + ||A||)^2
@@ -386,6 +390,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           } else {
             p = pt;
             rounds = 0;
+            x2 = lam_tau / (a.tau * a.tau);
             if constexpr (TZ && !DYN) {
               // G rows of this point that are not the shared interior row: rows [0, tz_j0) and
               // (tz_j1, n), then the interior row itself. They depend on z only, so every test of the
@@ -628,11 +633,14 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       }
       if (r == BIS_CONTINUE && rounds >= a.max_tests) r = BIS_FAIL;
       if (r != BIS_CONTINUE) {
-        if (gl == 0) {
+        // fallback points keep engine L's (non-converged) result unless the squared form is accurate here
+        if (gl == 0 && (!a.fallback || (r == BIS_DONE && 0.5 * (lo + hi) >= a.rmin2 * x2))) {
           const int64_t o = out_index(a.outidx, p);
           a.out[o] = sqrt(0.5 * (lo + hi));
           a.iters[o] = 1 + rounds * K;  // LDL^H tests incl. the classification test
           a.status[o] = (r == BIS_DONE) ? 1 : 3;
+        }
+        if (gl == 0) {
           atomicAdd(&a.counters[2], (unsigned long long)(1 + rounds * K));
           atomicAdd(&a.counters[3], 1ull);
         }
@@ -685,6 +693,7 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
     a.status[o] = (int8_t)stt;
     atomicAdd(&a.counters[5], (unsigned long long)(it > 0 ? it : 0));
     atomicAdd(&a.counters[6], 1ull);
+    if (stt == 3) a.listF[atomicAdd(&a.counters[8], 1ull)] = ~p;  // engine B retries it (fallback launch)
     p = -1;
     phase = 0;
   };

@@ -236,3 +236,23 @@ def test_partly_constant_band_long_boundary(gpu):
             A[i, j] += 0.3 * rng.standard_normal()
     zs = np.concatenate([core.make_grid(-1, 3, -3.5, 3.5, 6, 6).points().ravel(), [0.5 + 1.2j, 2.9 + 0.1j]])
     check(core.smin_many(A, zs), smin_restated(A, zs), np.linalg.norm(A, 2), "partly constant band")
+
+
+@pytest.mark.parametrize("offdiag", [0.0, 1e-6])
+def test_clustered_small_sigma_lanczos_fallback(gpu, offdiag):
+    """A tight cluster at sigma_min below the engine split: a diagonal (runtime-shape kernels) or
+    nearly diagonal tridiagonal band with entries 734.5 + 0.31 N(0,1), shifted next to the cluster.
+    Inverse Lanczos stagnates (regression: the old stop rule ended 8.5e-9 off, found by
+    tools/fuzz_parity.py); points that hit kmax are retried on engine B where the squared form is
+    accurate. sigma = min_j |z - a_jj| for the diagonal case."""
+    from oracle.sigma_oracle import smin_restated
+    rng = np.random.default_rng(4)
+    n = 160
+    a = 734.5 + 0.31 * rng.standard_normal(n)
+    A = np.diag(a) + offdiag * (np.diag(np.ones(n - 1), 1) + np.diag(np.ones(n - 1), -1))
+    zs = np.array([734.5318694864126 - 0.7180989702498619j, a[7] + 0.5j, a[3] - 0.9j, 734.0 + 0.3j])
+    got = core.smin_many(A, zs)
+    want = smin_restated(A, zs)
+    if offdiag == 0.0:
+        assert np.allclose(want, np.abs(zs[:, None] - a[None, :]).min(axis=1), rtol=1e-12)
+    check(got, want, np.linalg.norm(A, 2), f"clustered, offdiag={offdiag}")
