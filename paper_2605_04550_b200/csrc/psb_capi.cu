@@ -71,6 +71,7 @@ struct psb_handle {
   int n = 0, kl = 0, ku = 0;
   double2 dc{0.0, 0.0};  // engine-split scale (BisArgs): disc of A's diagonal, max off-diagonal column norm^2
   double dr = 0.0, offsq = 0.0;
+  double sscale = 1.0, zscale = 1.0;  // exact power-of-two problem scaling (psb_set_matrix)
   double anorm = 0.0;    // general-band kernels' split scale: sqrt(||A||_1 ||A||_inf) >= ||A||_2
   int tz_j0 = 1, tz_j1 = 0;  // interior rows sharing one G row (diagonal-constant band), empty by default
   // development knobs, read once at psb_create (A/B switches; defaults are the product path):
@@ -207,10 +208,26 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
                                       " ku=" + std::to_string(ku));
   const int nd = kl + ku + 1;
   typedef std::complex<double> cd;
-  const cd* A = reinterpret_cast<const cd*>(band);
-  for (int64_t t = 0; t < (int64_t)nd * n; t++)
-    if (!std::isfinite(A[t].real()) || !std::isfinite(A[t].imag()))
+  const cd* Ain = reinterpret_cast<const cd*>(band);
+  double amax = 0.0;
+  for (int64_t t = 0; t < (int64_t)nd * n; t++) {
+    if (!std::isfinite(Ain[t].real()) || !std::isfinite(Ain[t].imag()))
       return fail(h, PSB_ERR_PARAM, "matrix entries must be finite");
+    amax = std::max(amax, std::max(std::fabs(Ain[t].real()), std::fabs(Ain[t].imag())));
+  }
+  // Exact power-of-two scaling for matrices far from unit scale: the engines then run on A / 2^e and
+  // z / 2^e (|entries| <= 1) and sigma is multiplied back by 2^e, so the squared forms (G = M^H M,
+  // Lanczos on (M^H M)^-1) stay in range for |A| up to 1e+-300 (they overflowed from ~1e154). Inside
+  // [2^-64, 2^64] nothing is scaled: those matrices keep their validated bits (the scaled problem
+  // rounds the log-determinants of the secant differently, and moves the overflow edge of sigma).
+  const int ea = (amax > 0.0) ? std::ilogb(amax) : 0;
+  const int e2 = (ea > 64 || ea < -64) ? ea + 1 : 0;
+  h->sscale = std::ldexp(1.0, e2);
+  h->zscale = std::ldexp(1.0, -e2);
+  std::vector<cd> Asc((size_t)nd * n);
+  for (int64_t t = 0; t < (int64_t)nd * n; t++)
+    Asc[t] = cd(std::ldexp(Ain[t].real(), -e2), std::ldexp(Ain[t].imag(), -e2));
+  const cd* A = Asc.data();
   auto Aat = [&](int i, int c) -> cd {  // A[i, c]
     int d = c - i;
     if (d < -kl || d > ku || i < 0 || c < 0 || i >= n || c >= n) return cd(0, 0);
@@ -287,7 +304,7 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
   CK(cudaSetDevice(h->device));
   CK(h->Ab.ensure(sizeof(cd) * nd * n));
   CK(h->v1.ensure(sizeof(cd) * n * 33));
-  CK(cudaMemcpyAsync(h->Ab.p, band, sizeof(cd) * nd * n, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(h->Ab.p, A, sizeof(cd) * nd * n, cudaMemcpyHostToDevice, h->stream));
   // [0, n): v1; [n, 33n): v1 replicated per lane (v1rep[j*32 + lane]) for coalesced cp.async
   std::vector<cd> v1x((size_t)n * 33);
   for (int i = 0; i < n; i++) {
@@ -386,6 +403,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.n = n; ba.kl = kl; ba.ku = ku;
   ba.Ab = h->Ab.as<double2>(); ba.AHA = h->AHA.as<double2>(); ba.offmin = h->offmin.as<double>();
   ba.zs = d_zs; ba.outidx = d_outidx; ba.P = P;
+  ba.zscale = h->zscale; ba.sscale = h->sscale;
   ba.anorm = h->anorm; ba.dc = h->dc; ba.dr = h->dr; ba.offsq = h->offsq; ba.tau = opt.tau; ba.rtol = opt.bis_rtol;
   ba.force = opt.force_engine; ba.max_tests = 400;
   ba.out = d_out; ba.iters = d_iters; ba.status = d_status;
@@ -456,6 +474,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     la.v1 = dyn ? h->v1.as<double2>() : h->v1.as<double2>() + n;  // pipelined sweeps read the replicated copy
     la.v1b = h->v1.as<double2>();
     la.zs = d_zs; la.outidx = d_outidx; la.listA = h->listA.as<int64_t>(); la.counters = cnt; la.listF = h->listF.as<int64_t>();
+    la.zscale = h->zscale; la.sscale = h->sscale;
     la.out = d_out; la.iters = d_iters; la.status = d_status;
     la.scratch = h->scratch.as<double2>(); la.pivs = h->pivs.as<int>();
     la.warp_stride = warp_stride; la.piv_stride = piv_stride;

@@ -18,6 +18,7 @@ struct BisArgs {
   const int64_t* __restrict__ outidx;  // nullable: output index of point p
   int64_t P;
   double tau, rtol;
+  double zscale, sscale;          // exact power-of-two scaling: engines see z * zscale, report sigma * sscale
   const double* __restrict__ offmin;  // min(off-diagonal column, row norm^2) per index j (upper bound)
   double anorm;                   // general-band kernels: split scale S(z) = |z| + sqrt(||A||_1 ||A||_inf)
   double2 dc;                     // TZ kernels: engine-split scale T(z)^2 = (|z - dc| + dr)^2 + offsq >= max_j ||M e_j||^2
@@ -52,6 +53,7 @@ struct LanArgs {
   const int64_t* __restrict__ outidx;
   const int64_t* __restrict__ listA;
   unsigned long long* counters;   // [1] nA (read), [4] work, [5] lanczos steps, [6] nL, [8] n not converged
+  double zscale, sscale;          // exact power-of-two scaling (see BisArgs)
   int64_t* listF;                 // not-converged points (as ~p: forced bisection entries), counters[8] of them
   double* out;
   int32_t* iters;
@@ -371,7 +373,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           const int64_t entry = (a.mode == 0) ? q : a.listB[q];
           const bool forced = entry < 0;          // forced bisection of a point that failed classification
           const int64_t pt = forced ? ~entry : entry;
-          z = a.zs[pt];
+          z = cscale(a.zs[pt], a.zscale);
           // split at sigma = tau T(z): engine B's squared-form error is c eps T^2 / (2 sigma^2) relative
           // (c <= 0.6 measured), so sigma >= tau T keeps it below ~1e-10
           double lam_tau;
@@ -636,7 +638,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         // fallback points keep engine L's (non-converged) result unless the squared form is accurate here
         if (gl == 0 && (!a.fallback || (r == BIS_DONE && 0.5 * (lo + hi) >= a.rmin2 * x2))) {
           const int64_t o = out_index(a.outidx, p);
-          a.out[o] = sqrt(0.5 * (lo + hi));
+          a.out[o] = sqrt(0.5 * (lo + hi)) * a.sscale;
           a.iters[o] = 1 + rounds * K;  // LDL^H tests incl. the classification test
           a.status[o] = (r == BIS_DONE) ? 1 : 3;
         }
@@ -688,7 +690,7 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
 
   auto finish = [&](double sigma, int it, int stt) {
     const int64_t o = out_index(a.outidx, p);
-    a.out[o] = sigma;
+    a.out[o] = sigma * a.sscale;
     a.iters[o] = it;
     a.status[o] = (int8_t)stt;
     atomicAdd(&a.counters[5], (unsigned long long)(it > 0 ? it : 0));
@@ -710,7 +712,7 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
         const int64_t q = (int64_t)bq + rank;
         if (q < nA) {
           p = a.listA[q];
-          z = a.zs[p];
+          z = cscale(a.zs[p], a.zscale);
           phase = 1;
         }
       }

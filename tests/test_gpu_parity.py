@@ -256,3 +256,15 @@ def test_clustered_small_sigma_lanczos_fallback(gpu, offdiag):
     if offdiag == 0.0:
         assert np.allclose(want, np.abs(zs[:, None] - a[None, :]).min(axis=1), rtol=1e-12)
     check(got, want, np.linalg.norm(A, 2), f"clustered, offdiag={offdiag}")
+
+
+@pytest.mark.parametrize("scale", [1e-200, 1e200])
+def test_extreme_matrix_scales(gpu, scale):
+    """Matrices far from unit scale run on an exactly power-of-two-rescaled problem: the squared forms
+    (G = M^H M, (M^H M)^-1) overflowed from |A| ~ 1e154 (every sigma came back 0 at 1e200)."""
+    from oracle.sigma_oracle import smin_restated
+    A = configs.grcar_band(60).todense().real * scale
+    zs = core.make_grid(-1, 3, -3.5, 3.5, 7, 7).points().ravel() * scale
+    got, _, st = core.smin_many(A, zs, return_info=True)
+    assert np.all(st <= 1)
+    check(got, smin_restated(A, zs), np.linalg.norm(A, 2), f"scale {scale:g}")
