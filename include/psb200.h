@@ -47,7 +47,7 @@ extern "C" {
 typedef struct psb_handle psb_handle;
 
 typedef struct {
-  double tau;          /* engine split: sigma >= tau*X(z) -> bisection engine (default 1.5e-3). X is the
+  double tau;          /* engine split: sigma >= tau*X(z) -> bisection engine (default 1.5e-3 for n < 1000, else 1e-3). X is the
                           scale the bisection engine's G = (zI-A)^H (zI-A) is rounded at: for bands with a
                           diagonal-constant interior T(z), T^2 = (|z-c|+r)^2 + max off-diagonal column
                           norm^2 of A; otherwise S(z) = |z| + sqrt(||A||_1 ||A||_inf) */
