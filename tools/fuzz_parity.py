@@ -7,10 +7,11 @@ from oracle.sigma_oracle import floored_rel_err, smin_restated
 from paper_2605_04550_b200 import core
 
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
+big = len(sys.argv) > 3 and sys.argv[3] == 'big'  # include n = 1100 (the n >= 1000 engine split)
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 150
 worst, fails, t0 = 0.0, 0, time.time()
 for t in range(N):
-    n = int(rng.choice([2, 3, 5, 8, 17, 40, 90, 160, 300, 700]))
+    n = int(rng.choice([2, 3, 5, 8, 17, 40, 90, 160, 300, 700] + ([1100] if big else [])))
     wide = rng.random() < 0.15  # runtime-shape kernels (bands beyond the exact-shape table)
     kmax = min(16, n - 1) if wide else min(5, n - 1)
     kl, ku = int(rng.integers(0, kmax + 1)), int(rng.integers(0, kmax + 1))
