@@ -72,3 +72,47 @@ def sharded_full_pseudospectrum(A, grid, group=None, label: str = "matrix"):
     vals = sharded_sigma(grid.points().ravel(), lambda z: core.smin_many(A, z, label=label),
                          group=group, device=dev)
     return core.SigmaField(grid, vals.reshape(grid.shape))
+
+
+def sharded_restricted_sigma(grid, region: np.ndarray, evaluate: Callable[[np.ndarray], np.ndarray],
+                             group=None, device=None) -> np.ndarray:
+    """restricted_field's values (core.py:198-208) across the ranks of `group`: the region's points in
+    row-major order (core.py:204) are dealt cyclically, evaluated per rank and all-gathered; every
+    other grid point is NaN (core.py:203). Same bits as the single-GPU restricted map."""
+    region = np.asarray(region, dtype=bool)
+    if region.shape != tuple(grid.shape):
+        raise ValueError(f"region shape {region.shape} != grid shape {tuple(grid.shape)}")
+    idx = np.flatnonzero(region.ravel())
+    out = np.full(region.size, np.nan)
+    if idx.size:
+        out[idx] = sharded_sigma(grid.points().ravel()[idx], evaluate, group=group, device=device)
+    return out.reshape(grid.shape)
+
+
+def sharded_hybrid_pseudospectrum(bundle, A, grid, eps: float, group=None, probe_seed: int = 0,
+                                  stride: int = 4, label: str = "matrix"):
+    """hybrid_pseudospectrum (pipeline.py:273-297) across the ranks of `group` (guided
+    mode): every rank runs the predictor (K2) on its own GPU. That pass is deterministic, so all
+    ranks hold the same region without exchanging anything. Only the restricted σ sweep (K1) is
+    sharded, and its values are all-gathered."""
+    import time
+
+    import torch
+    from . import core, pipeline
+    if bundle.tau_star is None:
+        raise core.ParameterError("model bundle carries no calibrated threshold")
+    if eps <= 0:
+        raise core.ParameterError(f"eps must be positive, got {eps}")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t0 = time.perf_counter()
+    prob, n_evals = pipeline.hierarchical_predict(bundle, A, grid, stride=stride, probe_seed=probe_seed)
+    region = pipeline.predicted_region(prob, bundle.tau_star)
+    t_nn = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    vals = sharded_restricted_sigma(grid, region, lambda z: core.smin_many(A, z, label=label), group=group,
+                                    device=dev)
+    t_restricted = time.perf_counter() - t0
+    fld = core.SigmaField(grid, vals)
+    fld.eps = eps
+    return pipeline.HybridResult(field=fld, region=region, prob_field=prob, t_nn=t_nn,
+                                 t_restricted=t_restricted, nn_evaluations=n_evals)

@@ -119,3 +119,30 @@ def test_calibrate_threshold_matches_reference(gpu, gold, bundle, refpkg_any):
     assert rep.passed == want.passed and rep.tau_star == want.tau_star
     assert rep.passed == bool(z["passed"]) and rep.tau_star == float(z["tau_star"])
     assert np.max(np.abs(rep.recalls - z["recalls"])) <= 0.01
+
+
+def test_sharded_hybrid_equals_single_gpu(gpu, bundle):
+    """shard.sharded_hybrid_pseudospectrum on a one-rank NCCL group reproduces hybrid_pseudospectrum
+    bitwise (region, probabilities, restricted field): the only collective is the σ all-gather."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2605_04550_b200 import shard
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    c = configs.CONFIGS["C1"]
+    A = c.matrix().todense().real
+    one = pipeline.hybrid_pseudospectrum(bundle, A, c.grid, eps=0.01)
+    many = shard.sharded_hybrid_pseudospectrum(bundle, A, c.grid, eps=0.01)
+    assert np.array_equal(one.region, many.region)
+    assert np.array_equal(one.prob_field, many.prob_field)
+    assert np.array_equal(np.isnan(one.field.values), np.isnan(many.field.values))
+    assert np.array_equal(one.field.values[one.region], many.field.values[one.region])
+    assert one.nn_evaluations == many.nn_evaluations
+    dist.destroy_process_group()

@@ -61,3 +61,54 @@ def test_gloo_world2_gather(P):
     for rank, calls, vals in out:
         assert calls == [shard.shard_count(P, rank, 2)]  # each rank evaluated only its shard
         assert np.array_equal(vals, want)                 # and holds the full map after the gather
+
+
+class _Grid:  # minimal ComplexGrid stand-in (points, shape) for the CPU test
+    def __init__(self, ny, nx):
+        self.shape = (ny, nx)
+        x, y = np.linspace(-1, 1, nx), np.linspace(-2, 2, ny)
+        self._p = x[None, :] + 1j * y[:, None]
+
+    def points(self):
+        return self._p
+
+
+def _worker_restricted(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = _Grid(9, 13)
+    region = (np.arange(9 * 13).reshape(9, 13) * 7919) % 5 == 0
+    calls = []
+
+    def fake_sigma(z):
+        calls.append(z.size)
+        return np.abs(z) + 0.25 * z.imag
+    vals = shard.sharded_restricted_sigma(g, region, fake_sigma)
+    q.put((rank, calls, vals, region))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_restricted_map():
+    """Guided mode across ranks: the region's points are dealt cyclically in row-major
+    order (pseudospec core.py:204), each rank evaluates only its share, NaN elsewhere (core.py:203)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_restricted, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = _Grid(9, 13)
+    for rank, calls, vals, region in out:
+        k = int(region.sum())
+        assert calls == [shard.shard_count(k, rank, 2)]
+        want = np.full(g.shape, np.nan)
+        z = g.points()[region]
+        want[region] = np.abs(z) + 0.25 * z.imag
+        assert np.array_equal(np.isnan(vals), ~region)
+        assert np.array_equal(vals[region], want[region])
