@@ -116,3 +116,18 @@ def sharded_hybrid_pseudospectrum(bundle, A, grid, eps: float, group=None, probe
     fld.eps = eps
     return pipeline.HybridResult(field=fld, region=region, prob_field=prob, t_nn=t_nn,
                                  t_restricted=t_restricted, nn_evaluations=n_evals)
+
+
+def sharded_matrix_batch(matrices, grid, evaluate_field: Callable | None = None, group=None):
+    """σ maps of a batch of matrices on one grid (BASELINE C5: 64 matrices, 1024^2 grid each), matrices
+    dealt cyclically over the ranks of `group` (matrix i -> rank i mod N). Each rank
+    evaluates whole maps for its matrices; the maps stay on the rank that computed them, so the
+    result is {matrix index: SigmaField} for this rank's share and nothing is exchanged.
+    `evaluate_field(A, grid)` defaults to core.full_pseudospectrum."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if evaluate_field is None:
+        from . import core
+        evaluate_field = core.full_pseudospectrum
+    return {i: evaluate_field(matrices[i], grid) for i in shard_indices(len(matrices), rank, world).tolist()}

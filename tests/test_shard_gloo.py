@@ -112,3 +112,30 @@ def test_gloo_world2_restricted_map():
         want[region] = np.abs(z) + 0.25 * z.imag
         assert np.array_equal(np.isnan(vals), ~region)
         assert np.array_equal(vals[region], want[region])
+
+
+def _worker_batch(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mats = [np.full((2, 2), float(i)) for i in range(7)]
+    got = shard.sharded_matrix_batch(mats, None, evaluate_field=lambda A, g: float(A[0, 0]) * 10)
+    q.put((rank, got))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_matrix_batch():
+    """C5-style batches: matrix i goes to rank i mod N, each map computed exactly once."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_batch, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sorted(out[0]) == [0, 2, 4, 6] and sorted(out[1]) == [1, 3, 5]
+    assert all(v == 10 * i for part in out.values() for i, v in part.items())
