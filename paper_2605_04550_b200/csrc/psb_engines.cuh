@@ -342,7 +342,7 @@ template <int KL, int KU, bool DYN, int NP, int G, bool TZ>
 __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   constexpr int B = KL + KU;
   constexpr int K = NP * G;
-  constexpr bool SEC = (G == 1 && NP == 2);  // secant acceleration needs two probes per lane
+  constexpr bool SEC = (NP * G == 2);  // secant acceleration: two probes per round (one lane x 2, or 2 lanes x 1)
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;               // lane within the group
@@ -450,10 +450,10 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         if (dL > 1e-300 && dL < 700.0) {
           const double ls = lo + (lo - lp) / expm1(dL);
           if (ls > lo && ls < hi) {
-            lam[0] = ls;
             double p1 = ls + 0.1 * (ls - lo);
             if (!(p1 < hi)) p1 = 0.5 * (ls + hi);
-            lam[1] = p1;
+#pragma unroll
+            for (int q = 0; q < NP; q++) lam[q] = (gl * NP + q == 0) ? ls : p1;  // probe 0: ls, probe 1: p1
           }
         }
       }
@@ -594,6 +594,22 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       plo = fmax(plo, __shfl_xor_sync(FULL, plo, off, G));
       phi = fmin(phi, __shfl_xor_sync(FULL, phi, off, G));
     }
+    // the group's probes in ascending order i = gl * NP + q, with the log dets of the PD ones
+    double lamK[K], LK[K];
+    bool pdK[K];
+    if constexpr (SEC) {
+      if constexpr (G == 1) {
+#pragma unroll
+        for (int q = 0; q < NP; q++) { lamK[q] = lam[q]; pdK[q] = pd[q]; LK[q] = pd[q] ? ld[q].value() : 0.0; }
+      } else {  // G == 2, NP == 1: probe 0 on the group's even lane, probe 1 on the odd one
+        const double myL = pd[0] ? ld[0].value() : 0.0;
+        const double oL = __shfl_xor_sync(FULL, myL, 1, 2), olam = __shfl_xor_sync(FULL, lam[0], 1, 2);
+        const bool opd = __shfl_xor_sync(FULL, (int)pd[0], 1, 2) != 0;
+        lamK[0] = gl == 0 ? lam[0] : olam; lamK[1] = gl == 0 ? olam : lam[0];
+        pdK[0] = gl == 0 ? pd[0] : opd;    pdK[1] = gl == 0 ? opd : pd[0];
+        LK[0] = gl == 0 ? myL : oL;        LK[1] = gl == 0 ? oL : myL;
+      }
+    }
     if (me) {
       rounds++;
       int r = BIS_CONTINUE;
@@ -602,11 +618,10 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         // secant bookkeeping: keep the two highest PD points that carry a log det
         const double old_w = hi - lo;
 #pragma unroll
-        for (int q = 0; q < NP; q++) {
-          if (pd[q] && lam[q] > lo) {
-            const double Lq = ld[q].value();
+        for (int q = 0; q < K; q++) {
+          if (pdK[q] && lamK[q] > lo) {
             if (have_lo) { lp = lo; Lp = Llo; have_p = true; }
-            lo = lam[q]; Llo = Lq; have_lo = true;  // probes are ascending, so lo ends at the top PD one
+            lo = lamK[q]; Llo = LK[q]; have_lo = true;  // probes are ascending, so lo ends at the top PD one
           }
         }
         lo = fmax(lo, nlo);
