@@ -228,11 +228,6 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
   for (int64_t t = 0; t < (int64_t)nd * n; t++)
     Asc[t] = cd(std::ldexp(Ain[t].real(), -e2), std::ldexp(Ain[t].imag(), -e2));
   const cd* A = Asc.data();
-  auto Aat = [&](int i, int c) -> cd {  // A[i, c]
-    int d = c - i;
-    if (d < -kl || d > ku || i < 0 || c < 0 || i >= n || c >= n) return cd(0, 0);
-    return A[(int64_t)(d + kl) * n + i];
-  };
   const int b = kl + ku;
   CK(cudaSetDevice(h->device));
   // Engine-split scale T(z)^2 = (|z - dc| + dr)^2 + offsq bounds every column norm^2 of M = zI - A:
