@@ -268,3 +268,34 @@ def test_extreme_matrix_scales(gpu, scale):
     got, _, st = core.smin_many(A, zs, return_info=True)
     assert np.all(st <= 1)
     check(got, smin_restated(A, zs), np.linalg.norm(A, 2), f"scale {scale:g}")
+
+
+def test_randomised_band_sweep(gpu):
+    """A small slice of tools/fuzz_parity.py in the suite: random bands of many shapes (exact-shape and
+    runtime-shape kernels), structures (constant diagonals, noisy Toeplitz, general), real/complex,
+    scales 1e-3..1e6, with shifts next to eigenvalues, against zgesdd (floored gate)."""
+    from oracle.sigma_oracle import smin_restated
+    rng = np.random.default_rng(2026)
+    for t in range(40):
+        n = int(rng.choice([2, 3, 5, 8, 17, 40, 90, 160]))
+        kmax = min(16 if t % 7 == 0 else 5, n - 1)
+        kl, ku = int(rng.integers(0, kmax + 1)), int(rng.integers(0, kmax + 1))
+        cplx = bool(rng.random() < 0.5)
+        kind = ("toeplitz", "noisy", "general")[t % 3]
+        c = rng.standard_normal(kl + ku + 1) + (1j * rng.standard_normal(kl + ku + 1) if cplx else 0)
+        A = np.zeros((n, n), complex if cplx else float)
+        for d in range(-kl, ku + 1):
+            m = n - abs(d)
+            if m <= 0:
+                continue
+            if kind == "general":
+                v = rng.standard_normal(m) + (1j * rng.standard_normal(m) if cplx else 0)
+            else:
+                v = np.full(m, c[d + kl]) + (1e-3 * rng.standard_normal(m) if kind == "noisy" else 0)
+            A += np.diag(v, d)
+        A *= 10.0 ** rng.uniform(-3, 6)
+        ev = np.linalg.eigvals(A)
+        zs = (rng.uniform(ev.real.min() - 1, ev.real.max() + 1, 12)
+              + 1j * rng.uniform(ev.imag.min() - 1, ev.imag.max() + 1, 12))
+        zs = np.concatenate([zs, ev[: min(3, n)] * (1 + 1e-9)])
+        check(core.smin_many(A, zs), smin_restated(A, zs), np.linalg.norm(A, 2), f"sweep case {t} n={n} ({kl},{ku}) {kind}")
