@@ -382,7 +382,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   KPair kp;
   if (!pick(kl, ku, &kp)) return fail(h, PSB_ERR_CUDA, "library built without a kernel set for this band shape");
   const bool dyn = kp.kl < 0;
-  if (!dyn && h->tz_j0 <= h->tz_j1 && h->k_toeplitz) { kp.b = kp.bt; kp.bm = kp.bmt; }  // diagonal-constant row loop
+  if (!dyn && h->tz_j0 <= h->tz_j1 && h->k_toeplitz) { kp.b = kp.bt; kp.bm = kp.bmt; kp.bm2 = kp.bmt2; }  // diagonal-constant row loop
   h->stats = psb_stats{};
   h->stats.n_points = P;
   if (P == 0) return PSB_OK;
@@ -496,26 +496,43 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     // The block size is the one that fits the most threads there (points rarely outnumber threads by
     // much, so a second pass over a few leftover points would double the kernel). Launch shape never
     // changes a result: every sigma is a function of (A, z) only.
-    cudaFuncAttributes fb, fl;
-    CK(cudaFuncGetAttributes(&fb, kp.bm));
+    cudaFuncAttributes fl;
     if (nA > 0) CK(cudaFuncGetAttributes(&fl, kp.l));
     auto warp_regs = [](int r) { return (r * 32 + 255) / 256 * 256; };
-    int tpbB = 128, occShare = 1, occFull = 1;
-    int64_t best = -1;
-    for (int cand : {128, 64, 32}) {
-      if (h->k_btpb > 0 && cand != h->k_btpb) continue;
-      int occM = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, kp.bm, cand, 0));
-      occM = std::max(occM, 1);
-      int occ = occM;
-      if (nA > 0) {
-        const int regsL = warp_regs(fl.numRegs) * (int)(gridL > 0 ? kLWarpsPerBlock : 0);
-        const int regsB = warp_regs(fb.numRegs) * (cand / 32);
-        occ = std::max(1, std::min(occM, (65536 - regsL) / regsB));
+    // best block size for a variant: the most threads in what engine L leaves of each SM
+    struct Fit { int tpb, occ, occFull; int64_t threads; };
+    auto fit = [&](bis_fn f, Fit* out) -> cudaError_t {
+      cudaFuncAttributes fb;
+      cudaError_t e = cudaFuncGetAttributes(&fb, f);
+      if (e != cudaSuccess) return e;
+      *out = Fit{128, 1, 1, -1};
+      for (int cand : {128, 64, 32}) {
+        if (h->k_btpb > 0 && cand != h->k_btpb) continue;
+        int occM = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, f, cand, 0);
+        if (e != cudaSuccess) return e;
+        occM = std::max(occM, 1);
+        int occ = occM;
+        if (nA > 0) {
+          const int regsL = warp_regs(fl.numRegs) * (int)(gridL > 0 ? kLWarpsPerBlock : 0);
+          const int regsB = warp_regs(fb.numRegs) * (cand / 32);
+          occ = std::max(1, std::min(occM, (65536 - regsL) / regsB));
+        }
+        const int64_t thr = (int64_t)occ * cand * h->num_sms;
+        if (thr > out->threads) *out = Fit{cand, occ, occM, thr};
       }
-      const int64_t thr = (int64_t)occ * cand;
-      if (thr > best) { best = thr; tpbB = cand; occShare = occ; occFull = occM; }
-    }
+      return cudaSuccess;
+    };
+    // Wide variant (NP probes per lane) or the pair (two lanes per point, same bits): the pair when
+    // every point gets its two lanes in one pass (short lists: twice the threads on the same latency
+    // chain), the wide variant otherwise (long lists: one G-row formation serves both probes).
+    Fit fw, fp;
+    CK(fit(kp.bm, &fw));
+    CK(fit(kp.bm2, &fp));
+    const bool pair = kp.bm2 != kp.bm && 2 * nB <= fp.threads;  // (4,4) and the runtime shapes have one variant
+    if (pair) { kp.bm = kp.bm2; kp.np = 1; kp.g = 2; }
+    const Fit& fc = pair ? fp : fw;
+    const int tpbB = fc.tpb, occShare = fc.occ, occFull = fc.occFull;
     const int64_t wantB = (nB * kp.g + tpbB - 1) / tpbB;
     gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, wantB));
     // A second launch, queued behind engine L on its stream, takes the SM share engine L releases when

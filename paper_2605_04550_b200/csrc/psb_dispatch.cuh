@@ -13,9 +13,11 @@ typedef void (*bis_fn)(BisArgs);
 typedef void (*lan_fn)(LanArgs);
 // b: classification (NP = 1); bm: multisection (NP probes per thread); l: Lanczos engine.
 // bt / bmt: the same for bands with a diagonal-constant interior (TZ row loop).
-// (NP probes per lane) x (G lanes per point) are fixed per band shape: results must not depend on
-// the batch. lsmem: Lanczos ring bytes per warp. kl = -1 marks the runtime-shape set.
-struct KPair { int kl, ku; bis_fn b, bm, bt, bmt; lan_fn l; int lsmem; int np, g; };
+// bm2 / bmt2: the pair variant, the same K = 2 probes per round on two lanes (NP = 1, G = 2). Both
+// variants test the same shifts with the same arithmetic, so they return the same bits and the host
+// may pick either per launch (the pair for short lists, where each thread holds about one point).
+// np, g: the wide variant's split. lsmem: Lanczos ring bytes per warp. kl = -1: runtime-shape set.
+struct KPair { int kl, ku; bis_fn b, bm, bt, bmt, bm2, bmt2; lan_fn l; int lsmem; int np, g; };
 
 void register_shape(const KPair& k);  // defined in psb_capi.cu
 
