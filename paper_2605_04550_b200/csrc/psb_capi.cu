@@ -75,13 +75,14 @@ struct psb_handle {
   double anorm = 0.0;    // general-band kernels' split scale: sqrt(||A||_1 ||A||_inf) >= ||A||_2
   int tz_j0 = 1, tz_j1 = 0;  // interior rows sharing one G row (diagonal-constant band), empty by default
   // development knobs, read once at psb_create (A/B switches; defaults are the product path):
-  //   PSB_TAU=x default engine split, PSB_NOBEXP=1 no second engine-B launch, PSB_BTPB=n engine-B block size, PSB_NOSEC=1 plain multisection, PSB_NOTZ=1 per-row G formation, PSB_LWARPS=N cap on
+  //   PSB_TAU=x default engine split, PSB_BVARIANT=1/2 force the wide / pair bisection variant, PSB_NOBEXP=1 no second engine-B launch, PSB_BTPB=n engine-B block size, PSB_NOSEC=1 plain multisection, PSB_NOTZ=1 per-row G formation, PSB_LWARPS=N cap on
   //   Lanczos warps, PSB_PROF=1 per-phase clock64 counters of the Lanczos kernel (stderr)
   bool k_secant = true, k_toeplitz = true, k_prof = false;
   long long k_lwarps = 0;
   int k_btpb = 128;
   double k_tau = 0.0;
   bool k_bexpand = true, k_fallback = true;
+  int k_bvariant = 0;
   bool have_matrix = false;
   DevBuf Ab, AHA, v1, offmin, gbuf, listF;
   // per call
@@ -164,6 +165,7 @@ int psb_create(int device, psb_handle** out) {
   h->k_prof = getenv("PSB_PROF") != nullptr;
   h->k_bexpand = getenv("PSB_NOBEXP") == nullptr;
   h->k_fallback = getenv("PSB_NOFALLBACK") == nullptr;
+  h->k_bvariant = getenv("PSB_BVARIANT") ? atoi(getenv("PSB_BVARIANT")) : 0;
   h->k_tau = getenv("PSB_TAU") ? atof(getenv("PSB_TAU")) : 0.0;  // dev: default engine split
   h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 0;  // 0: pick per launch
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
@@ -529,7 +531,8 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     Fit fw, fp;
     CK(fit(kp.bm, &fw));
     CK(fit(kp.bm2, &fp));
-    const bool pair = kp.bm2 != kp.bm && 2 * nB <= fp.threads;  // (4,4) and the runtime shapes have one variant
+    const bool pair = kp.bm2 != kp.bm && (h->k_bvariant == 2 || (h->k_bvariant == 0 && 2 * nB <= fp.threads));
+    // ((4,4) and the runtime shapes have one variant; PSB_BVARIANT=1/2 forces wide/pair for tests)
     if (pair) { kp.bm = kp.bm2; kp.np = 1; kp.g = 2; }
     const Fit& fc = pair ? fp : fw;
     const int tpbB = fc.tpb, occShare = fc.occ, occFull = fc.occFull;

@@ -299,3 +299,25 @@ def test_randomised_band_sweep(gpu):
               + 1j * rng.uniform(ev.imag.min() - 1, ev.imag.max() + 1, 12))
         zs = np.concatenate([zs, ev[: min(3, n)] * (1 + 1e-9)])
         check(core.smin_many(A, zs), smin_restated(A, zs), np.linalg.norm(A, 2), f"sweep case {t} n={n} ({kl},{ku}) {kind}")
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_engine_b_variants_bitwise_equal(gpu, tmp_path, name):
+    """The wide (NP = 2) and pair (NP = 1, G = 2) bisection variants probe the same shifts with the same
+    arithmetic, so the host's per-launch choice between them must not change a bit (PSB_BVARIANT,
+    read at handle creation: 1 wide, 2 pair). C1 (short list, pair by default) and C3 (long list)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = ("import sys, numpy as np; sys.path.insert(0, '.'); from paper_2605_04550_b200 import configs, core; "
+            f"c = configs.CONFIGS['{name}']; z = c.grid.points().ravel()[::3]; "
+            "np.save(sys.argv[1], core.smin_many(c.matrix(), z))")
+    outs = []
+    for v in ("1", "2"):
+        env = {**os.environ, "PSB_BVARIANT": v}
+        path = tmp_path / f"v{v}.npy"
+        subprocess.run([sys.executable, "-c", code, str(path)], check=True, env=env,
+                       cwd=str(Path(__file__).resolve().parents[1]))
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
