@@ -502,12 +502,12 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     if (nA > 0) CK(cudaFuncGetAttributes(&fl, kp.l));
     auto warp_regs = [](int r) { return (r * 32 + 255) / 256 * 256; };
     // best block size for a variant: the most threads in what engine L leaves of each SM
-    struct Fit { int tpb, occ, occFull; int64_t threads; };
+    struct Fit { int tpb, occ, occFull; int64_t threads; int wregs; };
     auto fit = [&](bis_fn f, Fit* out) -> cudaError_t {
       cudaFuncAttributes fb;
       cudaError_t e = cudaFuncGetAttributes(&fb, f);
       if (e != cudaSuccess) return e;
-      *out = Fit{128, 1, 1, -1};
+      *out = Fit{128, 1, 1, -1, warp_regs(fb.numRegs)};
       for (int cand : {128, 64, 32}) {
         if (h->k_btpb > 0 && cand != h->k_btpb) continue;
         int occM = 0;
@@ -521,7 +521,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
           occ = std::max(1, std::min(occM, (65536 - regsL) / regsB));
         }
         const int64_t thr = (int64_t)occ * cand * h->num_sms;
-        if (thr > out->threads) *out = Fit{cand, occ, occM, thr};
+        if (thr > out->threads) *out = Fit{cand, occ, occM, thr, warp_regs(fb.numRegs)};
       }
       return cudaSuccess;
     };
@@ -543,13 +543,26 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     // full occupancy instead of the share it had next to engine L.
     // Only for long lists (>= 4 points per thread after the expansion): with ~1-2 points per thread the
     // late starters' last points stretch the tail by a point's latency (C3: +4%; C5: -15%).
+    bis_fn fB2 = kp.bm;
+    int tpb2 = tpbB, g2 = kp.g;
     if (nA > 0 && gridL > 0 && h->k_bexpand) {
       const int64_t extra = std::max<int64_t>(0, std::min<int64_t>((int64_t)occFull * h->num_sms, wantB) - gridB);
-      if (nB * kp.g >= 4 * (gridB + extra) * tpbB) gridB2 = extra;
+      if (nB * kp.g >= 4 * (gridB + extra) * tpbB) {
+        gridB2 = extra;  // long list: the same (wide) variant at full occupancy (C5 1157 -> 975 ms)
+      } else if (!pair && kp.bm2 != kp.bm && nB * kp.g >= 2 * gridB * tpbB) {
+        // 2-4 points per thread: the pair variant, whose late points finish in about half the latency
+        // (C3 15.1 -> 14.8 ms; on C5's long list it lost to the wide expansion, 975 -> 1064 ms)
+        const int wB1 = (int)((gridB + h->num_sms - 1) / h->num_sms) * (tpbB / 32);  // B1 warps per SM
+        const int used = ((wB1 + 3) / 4) * fw.wregs;                                  // per 16K slice
+        const int per_slice = std::max(0, (16384 - used) / fp.wregs);
+        const int64_t ex2 = std::min<int64_t>((int64_t)4 * per_slice * h->num_sms, (2 * nB + 31) / 32);
+        if (ex2 > 0) { gridB2 = ex2; fB2 = kp.bm2; tpb2 = 32; g2 = 2; }
+      }
     }
+    (void)g2;
     ba.mode = 1;
     ba.max_tests = 200;
-    ba.gb_T = (gridB + gridB2) * tpbB;
+    ba.gb_T = gridB * tpbB + gridB2 * tpb2;
     ba.tid_base = 0;
     if (tzk) {  // after the host round trip the classification kernel is done: resizing is safe
       CK(h->gbuf.ensure(sizeof(double2) * (size_t)(ba.nb + 1) * (kl + ku + 1) * (size_t)ba.gb_T));
@@ -565,7 +578,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     if (gridB2 > 0) {
       BisArgs b2 = ba;
       b2.tid_base = gridB * tpbB;
-      kp.bm<<<(unsigned)gridB2, tpbB, 0, h->stream2>>>(b2);
+      fB2<<<(unsigned)gridB2, tpb2, 0, h->stream2>>>(b2);
       CK(cudaGetLastError());
       CK(cudaEventRecord(h->ev[6], h->stream2));
     }
