@@ -83,6 +83,8 @@ struct psb_handle {
   double k_tau = 0.0;
   bool k_bexpand = true, k_fallback = true;
   int k_bvariant = 0;
+  struct FitEntry { const void* f; int lkey, btpb, tpb, occ, occFull; int64_t threads; int wregs; };
+  std::vector<FitEntry> fit_cache;  // engine-B launch shapes per (kernel, engine-L share)
   bool have_matrix = false;
   DevBuf Ab, AHA, v1, offmin, gbuf, listF;
   // per call
@@ -503,7 +505,15 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     auto warp_regs = [](int r) { return (r * 32 + 255) / 256 * 256; };
     // best block size for a variant: the most threads in what engine L leaves of each SM
     struct Fit { int tpb, occ, occFull; int64_t threads; int wregs; };
+    const int regsLkey = (nA > 0) ? warp_regs(fl.numRegs) * (int)(gridL > 0 ? kLWarpsPerBlock : 0) : -1;
     auto fit = [&](bis_fn f, Fit* out) -> cudaError_t {
+      // memoised per (kernel, engine-L register share): the attribute and occupancy queries cost
+      // microseconds per call, a visible share of a small grid's step
+      for (const auto& c : h->fit_cache)
+        if (c.f == (const void*)f && c.lkey == regsLkey && c.btpb == h->k_btpb) {
+          *out = Fit{c.tpb, c.occ, c.occFull, c.threads, c.wregs};
+          return cudaSuccess;
+        }
       cudaFuncAttributes fb;
       cudaError_t e = cudaFuncGetAttributes(&fb, f);
       if (e != cudaSuccess) return e;
@@ -523,6 +533,8 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
         const int64_t thr = (int64_t)occ * cand * h->num_sms;
         if (thr > out->threads) *out = Fit{cand, occ, occM, thr, warp_regs(fb.numRegs)};
       }
+      h->fit_cache.push_back({(const void*)f, regsLkey, h->k_btpb, out->tpb, out->occ, out->occFull, out->threads,
+                              out->wregs});
       return cudaSuccess;
     };
     // Wide variant (NP probes per lane) or the pair (two lanes per point, same bits): the pair when
