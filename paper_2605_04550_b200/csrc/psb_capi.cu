@@ -85,6 +85,8 @@ struct psb_handle {
   int k_bvariant = 0;
   struct FitEntry { const void* f; int lkey, btpb, tpb, occ, occFull; int64_t threads; int wregs; };
   std::vector<FitEntry> fit_cache;  // engine-B launch shapes per (kernel, engine-L share)
+  struct LanEntry { const void* f; int lsmem, occ, regs; };
+  std::vector<LanEntry> lan_cache;  // engine-L occupancy and registers per kernel
   bool have_matrix = false;
   DevBuf Ab, AHA, v1, offmin, gbuf, listF;
   // per call
@@ -460,8 +462,18 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   int64_t gridL = 0;
   int occL = 0;
   if (nA > 0) {
-    if (lsmem > 48 * 1024) CK(cudaFuncSetAttribute(kp.l, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occL, kp.l, 32 * kLWarpsPerBlock, lsmem));
+    // memoised per kernel: attribute set-up and the occupancy query once per handle
+    auto it = std::find_if(h->lan_cache.begin(), h->lan_cache.end(),
+                           [&](const psb_handle::LanEntry& c) { return c.f == (const void*)kp.l && c.lsmem == lsmem; });
+    if (it != h->lan_cache.end()) {
+      occL = it->occ;
+    } else {
+      if (lsmem > 48 * 1024) CK(cudaFuncSetAttribute(kp.l, cudaFuncAttributeMaxDynamicSharedMemorySize, lsmem));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occL, kp.l, 32 * kLWarpsPerBlock, lsmem));
+      cudaFuncAttributes fa;
+      CK(cudaFuncGetAttributes(&fa, kp.l));
+      h->lan_cache.push_back({(const void*)kp.l, lsmem, occL, fa.numRegs});
+    }
     occL = std::max(occL, 1);
     const double budget = 24.0 * (1ull << 30);  // scratch budget (HBM is 180 GB)
     const double per_warp = warp_stride * 16.0 + piv_stride * 4.0;
@@ -500,8 +512,11 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     // The block size is the one that fits the most threads there (points rarely outnumber threads by
     // much, so a second pass over a few leftover points would double the kernel). Launch shape never
     // changes a result: every sigma is a function of (A, z) only.
-    cudaFuncAttributes fl;
-    if (nA > 0) CK(cudaFuncGetAttributes(&fl, kp.l));
+    cudaFuncAttributes fl{};
+    if (nA > 0) {
+      for (const auto& c : h->lan_cache)
+        if (c.f == (const void*)kp.l) fl.numRegs = c.regs;
+    }
     auto warp_regs = [](int r) { return (r * 32 + 255) / 256 * 256; };
     // best block size for a variant: the most threads in what engine L leaves of each SM
     struct Fit { int tpb, occ, occFull; int64_t threads; int wregs; };
