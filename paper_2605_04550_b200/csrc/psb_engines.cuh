@@ -328,16 +328,17 @@ struct RingDepth {
 __device__ __forceinline__ int64_t out_index(const int64_t* outidx, int64_t p) { return outidx ? outidx[p] : p; }
 
 // ----------------------------------------------------------------- engine B kernel
-// mode 0 (NP = G = 1): classification — one LDL^H test per point at lambda = (tau S)^2; PD points
-//   go to listB (sigma >= tau S), the rest to listA (Lanczos engine).
+// mode 0 (NP = G = 1): classification — one LDL^H test per point at lambda = (tau X(z))^2; PD points
+//   go to listB (sigma >= tau X), the rest to listA (Lanczos engine).
 // mode 1: multisection of the listB points. A group of G lanes owns one point and every lane runs NP
-//   independent LDL^H chains (sharing the G-row formation), so a round tests K = G*NP shifts:
-//   search rounds probe lo*4^(i+1), then the bracket [lo, hi] is cut at lo + (hi-lo)(i+1)/(K+1).
-//   The group keeps [max PD probe, min non-PD probe] (shuffle reductions), so the bracket shrinks
-//   (K+1)-fold per round. (G, NP) depend only on the band shape, never on the batch, so every sigma
-//   is a pure function of (A, z).
-// TZ: the band has a diagonal-constant interior (a.tz_j0 <= a.tz_j1) whose G row is formed once per
-// round; the general-band row loop is a separate instantiation so each gets its own register budget.
+//   independent LDL^H chains (sharing the G-row formation), so a round tests K = G*NP shifts: search
+//   rounds probe upward (or geometrically inside [lo, U^2]), then the bracket [lo, hi] is cut at
+//   lo + (hi-lo)(i+1)/(K+1) or at the secant probes (K = 2). The group keeps [max PD probe, min non-PD
+//   probe] (shuffle reductions). Probe i = gl*NP + q is the same shift for (NP, G) = (2, 1) and (1, 2),
+//   so those two variants return the same bits and the host may launch either; every sigma is a pure
+//   function of (A, z).
+// TZ: the band has a diagonal-constant interior (a.tz_j0 <= a.tz_j1) whose G rows are formed once per
+// point; the general-band row loop is a separate instantiation so each gets its own register budget.
 template <int KL, int KU, bool DYN, int NP, int G, bool TZ>
 __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   constexpr int B = KL + KU;
