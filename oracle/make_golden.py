@@ -290,6 +290,56 @@ def gen_calib():
     print("calib: passed", rep.passed, rep.tau_star, flush=True)
 
 
+def gen_c5_strat(maps_path="gpurun_out/c5_maps.npz", per_matrix=64, procs=7):
+    """C5 parity pinned on meaningful points: for each of 4 matrices, 64 grid shifts stratified by what
+    they exercise, with sigma from the restated zgesdd oracle (complex A). Strata (per matrix):
+      24  bisection-engine points with sigma >= the parity floor 1e-5 ||A||_2 (the general-band kernel)
+      16  points straddling the engine split sigma = tau S(z) (tau = 1e-3, S = |z| + sqrt(||A||_1 ||A||_inf)),
+          8 on each side
+      12  points within 20% of an eps level (1e-1, 1e-2, 1e-3; 4 each)
+      12  Lanczos-engine points with sigma >= the floor
+    The strata are chosen from a full C5 sigma map computed by this repo's GPU evaluator
+    (tools/c5_maps.py); that map only picks *which* shifts to test — every fixture value is the
+    oracle's zgesdd (oracle/sigma_oracle.smin_restated)."""
+    cfg = configs.CONFIGS["C5"]
+    z = np.load(maps_path)
+    pts = cfg.grid.points().ravel()
+    rows = []
+    for m in (int(x) for x in z["matrices"]):
+        A = cfg.matrix(m)
+        Ad = A.todense()
+        n2 = np.linalg.norm(Ad, 2)
+        floor = 1e-5 * n2
+        anorm = np.sqrt(np.abs(Ad).sum(0).max() * np.abs(Ad).sum(1).max())
+        s = z[f"sigma_{m}"].astype(float).ravel()
+        st = z[f"status_{m}"].ravel()
+        split = 1e-3 * (np.abs(pts) + anorm)
+        rng = np.random.default_rng(np.random.PCG64(configs.mix64(5005, m)))
+        pick = []
+
+        def take(cand, k):
+            cand = np.setdiff1d(cand, np.array(pick, dtype=np.int64))
+            sel = rng.choice(cand, size=min(k, cand.size), replace=False) if cand.size else np.zeros(0, int)
+            pick.extend(int(c) for c in sel)
+
+        take(np.flatnonzero((st == 1) & (s >= floor)), 24)
+        take(np.flatnonzero((s > 0.5 * split) & (s < split)), 8)
+        take(np.flatnonzero((s >= split) & (s < 2 * split)), 8)
+        for e in (1e-1, 1e-2, 1e-3):
+            take(np.flatnonzero(np.abs(s / e - 1) < 0.2), 4)
+        take(np.flatnonzero((st == 0) & (s >= floor)), per_matrix - len(pick))
+        idx = np.sort(np.array(pick, dtype=np.int64))
+        zs = pts[idx]
+        t = time.time()
+        want = _pool(_restated_chunk, Ad, zs, procs=procs)
+        rows.append((m, idx, zs, want, n2))
+        print("C5 strat", m, idx.size, "above floor", int((want >= floor).sum()), time.time() - t, flush=True)
+        np.savez_compressed(GOLD / "c5_strat.npz", matrices=np.array([r[0] for r in rows]),
+                            idx=np.stack([r[1] for r in rows]), zs=np.stack([r[2] for r in rows]),
+                            sigma=np.stack([r[3] for r in rows]), norm2=np.array([r[4] for r in rows]),
+                            tau=np.array(1e-3))
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("sigma", "all"):
@@ -306,3 +356,5 @@ if __name__ == "__main__":
         gen_io()
     if what in ("calib", "all"):
         gen_calib()
+    if what == "c5strat":
+        gen_c5_strat()

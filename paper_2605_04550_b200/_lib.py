@@ -142,10 +142,28 @@ class Handle:
 _handles: dict[int, Handle] = {}
 
 
+def default_device() -> int:
+    """The caller's device: $PSB200_DEVICE, else torch's current device when torch has already
+    initialised CUDA in this process (a torch.distributed rank bound with torch.cuda.set_device),
+    else $LOCAL_RANK (one process per GPU under torchrun), else 0."""
+    env = os.environ.get("PSB200_DEVICE")
+    if env is not None:
+        return int(env)
+    import sys
+    torch = sys.modules.get("torch")
+    if torch is not None:
+        try:
+            if torch.cuda.is_initialized():
+                return int(torch.cuda.current_device())
+        except Exception:
+            pass
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
 def handle(device: int | None = None) -> Handle:
-    """Process-wide handle for `device` (default: $PSB200_DEVICE or 0)."""
+    """Process-wide handle for `device` (default: `default_device()`)."""
     if device is None:
-        device = int(os.environ.get("PSB200_DEVICE", "0"))
+        device = default_device()
     with _lib_lock:
         h = _handles.get(device)
     if h is None:

@@ -202,6 +202,7 @@ def _set_matrix(h: _lib.Handle, A):
     key = (n, kl, ku, hashlib.blake2b(band.tobytes(), digest_size=16).digest())
     if h._matrix_key == key:
         return n
+    h._matrix_key = None  # a failed upload leaves no matrix the key could vouch for
     rc = h.lib.psb_set_matrix(h.h, band.ctypes.data_as(C.c_void_p), n, kl, ku)
     if rc == _lib.PSB_ERR_PARAM:
         raise ParameterError(h.error())
@@ -240,13 +241,19 @@ def last_stats() -> dict:
 
 
 def smin_many(A, zs: np.ndarray, label: str = "matrix", chunk: int = 512, *,
-              opts: _lib.Opts | None = None, return_info: bool = False):
-    """σ_min(z I - A) for a 1-D array of shift points (core.py:141-168)."""
+              opts: _lib.Opts | None = None, return_info: bool = False, device: int | None = None):
+    """σ_min(z I - A) for a 1-D array of shift points (core.py:141-168).
+
+    `device`: the CUDA device to run on (default `_lib.default_device()`: the rank's device
+    under torch.distributed). A non-finite shift raises NumericalError naming its index and z,
+    as the reference's LinAlgError path does (core.py:157-166)."""
     zs = np.ascontiguousarray(np.asarray(zs, dtype=complex).ravel())
     band = as_band(A)  # validate on the host first (ParameterError without touching the device)
-    if not np.all(np.isfinite(zs)):
-        raise ParameterError("shift points must be finite")
-    h = _lib.handle()
+    bad = np.flatnonzero(~np.isfinite(zs))
+    if bad.size:
+        i = int(bad[0])
+        raise NumericalError(f"SVD failed to converge on {label} at point index {i}, z={zs[i]}")
+    h = _lib.handle(device)
     with h.lock:
         _set_matrix(h, band)
         P = zs.size
@@ -266,16 +273,19 @@ def smin_many(A, zs: np.ndarray, label: str = "matrix", chunk: int = 512, *,
     return out
 
 
-def smin_at(A, z: complex, label: str = "matrix") -> float:
+def smin_at(A, z: complex, label: str = "matrix", *, device: int | None = None) -> float:
     """σ_min of z I - A at one point (core.py:131-138); identical bits to smin_many."""
-    return float(smin_many(A, np.array([z], dtype=complex), label=label)[0])
+    z = complex(z)
+    if not np.isfinite(z):
+        raise NumericalError(f"SVD failed to converge on {label} at z={z}")
+    return float(smin_many(A, np.array([z], dtype=complex), label=label, device=device)[0])
 
 
-def _grid_call(A, grid: ComplexGrid, region, label, opts=None):
+def _grid_call(A, grid: ComplexGrid, region, label, opts=None, device=None):
     xs = np.ascontiguousarray(grid.xs())
     ys = np.ascontiguousarray(grid.ys())
     band = as_band(A)
-    h = _lib.handle()
+    h = _lib.handle(device)
     with h.lock:
         _set_matrix(h, band)
         out = np.empty(grid.shape)
@@ -296,18 +306,19 @@ def _grid_call(A, grid: ComplexGrid, region, label, opts=None):
 
 
 def full_pseudospectrum(A, grid: ComplexGrid, label: str = "matrix",
-                        workers: int = 1, *, opts: _lib.Opts | None = None) -> SigmaField:
+                        workers: int = 1, *, opts: _lib.Opts | None = None,
+                        device: int | None = None) -> SigmaField:
     """σ_min at every grid point (core.py:177-195). `workers` is ignored (one GPU process)."""
-    return SigmaField(grid, _grid_call(A, grid, None, label, opts))
+    return SigmaField(grid, _grid_call(A, grid, None, label, opts, device))
 
 
 def restricted_field(A, grid: ComplexGrid, region: np.ndarray, label: str = "matrix", *,
-                     opts: _lib.Opts | None = None) -> SigmaField:
+                     opts: _lib.Opts | None = None, device: int | None = None) -> SigmaField:
     """σ_min only on the True points of `region`; the rest stays NaN (core.py:198-208)."""
     region = _check_mask(region, grid.shape)
     if not region.any():
         return SigmaField(grid, np.full(grid.shape, np.nan))
-    return SigmaField(grid, _grid_call(A, grid, region, label, opts))
+    return SigmaField(grid, _grid_call(A, grid, region, label, opts, device))
 
 
 def sensitive_zone(field: SigmaField, eps: float) -> np.ndarray:

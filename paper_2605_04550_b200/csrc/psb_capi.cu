@@ -98,6 +98,20 @@ struct psb_handle {
   psb_stats stats{};
 };
 
+// Every entry point runs on the handle's device and gives the caller's current device back on
+// return (a torch.distributed rank bound to cuda:r must not find itself on cuda:0 afterwards).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 static int fail(psb_handle* h, int code, const std::string& msg) {
   if (h) h->err = msg;
   return code;
@@ -160,6 +174,7 @@ int psb_create(int device, psb_handle** out) {
   cudaError_t e = cudaGetDeviceCount(&count);
   if (e != cudaSuccess || count == 0) return PSB_ERR_CUDA;
   if (device < 0 || device >= count) return PSB_ERR_PARAM;
+  DeviceGuard dg(device);
   psb_handle* h = new psb_handle();
   h->device = device;
   if (cudaSetDevice(device) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
@@ -182,7 +197,7 @@ int psb_create(int device, psb_handle** out) {
 
 void psb_destroy(psb_handle* h) {
   if (!h) return;
-  cudaSetDevice(h->device);
+  DeviceGuard dg(h->device);
   DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->v1, &h->offmin, &h->gbuf, &h->listF, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
                     &h->counters, &h->scratch, &h->pivs, &h->dynL, &h->dynD, &h->xs, &h->ys, &h->params,
                     &h->feat, &h->eig, &h->prob, &h->region, &h->idx};
@@ -205,6 +220,9 @@ int psb_get_stats(const psb_handle* h, psb_stats* out) {
 int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int32_t ku) {
   if (!h) return PSB_ERR_PARAM;
   std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard dg(h->device);
+  // no matrix until every upload below succeeded (a failed call must not leave a mixed state)
+  h->have_matrix = false;
   if (!band) return fail(h, PSB_ERR_PARAM, "band is NULL");
   if (n < 2) return fail(h, PSB_ERR_PARAM, "expected a square matrix with n >= 2, got n=" + std::to_string(n));
   if (kl < 0 || ku < 0 || kl >= n || ku >= n)
@@ -703,7 +721,7 @@ int psb_smin_points_device(psb_handle* h, const double* d_zs, int64_t P, const p
   std::lock_guard<std::mutex> lk(h->mu);
   if (!h->have_matrix) return fail(h, PSB_ERR_PARAM, "no matrix set");
   if (P < 0 || (P > 0 && (!d_zs || !d_sigma))) return fail(h, PSB_ERR_PARAM, "bad point arguments");
-  CK(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
   cudaStream_t st = stream ? (cudaStream_t)stream : h->stream;
   if (!d_iters) { CK(h->iters.ensure(sizeof(int32_t) * std::max<int64_t>(P, 1))); d_iters = h->iters.as<int32_t>(); }
   if (!d_status) { CK(h->status.ensure(sizeof(int8_t) * std::max<int64_t>(P, 1))); d_status = h->status.as<int8_t>(); }
@@ -718,9 +736,13 @@ int psb_smin_points(psb_handle* h, const double* zs, int64_t P, const psb_opts* 
   if (!h->have_matrix) return fail(h, PSB_ERR_PARAM, "no matrix set");
   if (P < 0 || (P > 0 && (!zs || !sigma))) return fail(h, PSB_ERR_PARAM, "bad point arguments");
   if (P == 0) { h->stats = psb_stats{}; return PSB_OK; }
+  // a non-finite shift is the reference's LinAlgError path: NumericalError with the index (core.py:157-166)
   for (int64_t i = 0; i < 2 * P; i++)
-    if (!std::isfinite(zs[i])) return fail(h, PSB_ERR_PARAM, "shift points must be finite");
-  CK(cudaSetDevice(h->device));
+    if (!std::isfinite(zs[i])) {
+      if (fail_index) *fail_index = i / 2;
+      return fail(h, PSB_ERR_NUMERICAL, "non-finite shift point");
+    }
+  DeviceGuard dg(h->device);
   cudaStream_t st = h->stream;
   CK(h->zs.ensure(sizeof(double2) * P));
   CK(h->out.ensure(sizeof(double) * P));
@@ -753,7 +775,7 @@ int psb_smin_grid(psb_handle* h, const double* xs, int32_t nx, const double* ys,
   if (!h->have_matrix) return fail(h, PSB_ERR_PARAM, "no matrix set");
   if (!xs || !ys || !sigma || nx < 1 || ny < 1) return fail(h, PSB_ERR_PARAM, "bad grid arguments");
   const int64_t N = (int64_t)nx * ny;
-  CK(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
   cudaStream_t st = h->stream;
   // pinned staging: [xs | ys | idx (restricted) | sigma | iters | status]
   const size_t ox = 0, oy = ox + 8 * (size_t)nx, oidx = oy + 8 * (size_t)ny;
@@ -840,7 +862,7 @@ extern "C" {
 int psb_fp64_peak(psb_handle* h, double* tflops) {
   if (!h || !tflops) return PSB_ERR_PARAM;
   std::lock_guard<std::mutex> lk(h->mu);
-  CK(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
   cudaStream_t st = h->stream;
   CK(h->prob.ensure(64));
   const int iters = 4096, blocks = h->num_sms * 8, threads = 256;
@@ -865,7 +887,7 @@ int psb_predict_points(psb_handle* h, const double* params, const double* mean33
   if (!params || !mean33 || !std33 || !f30 || !eig || !eig_mean || n_eig < 1 || P < 0 || (P > 0 && (!zs || !prob)))
     return fail(h, PSB_ERR_PARAM, "bad predictor arguments");
   if (P == 0) return PSB_OK;
-  CK(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
   cudaStream_t st = h->stream;
   const size_t npar = MlpOff::total;
   CK(h->params.ensure(sizeof(double) * npar));
@@ -909,7 +931,7 @@ int psb_region_select(psb_handle* h, const double* prob, int32_t ny, int32_t nx,
   if (!prob || !region || ny < 1 || nx < 1 || k < 1 || (k % 2) == 0)
     return fail(h, PSB_ERR_PARAM, "bad region arguments");
   const int64_t N = (int64_t)ny * nx;
-  CK(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
   cudaStream_t st = h->stream;
   CK(h->prob.ensure(sizeof(double) * N));
   CK(h->region.ensure(N));
@@ -939,7 +961,7 @@ int psb_recall_sweep(psb_handle* h, const double* prob, const uint8_t* truth, in
     for (int t = 0; t < n_tau; t++) recall[t] = 1.0;
     return PSB_OK;
   }
-  CK(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
   cudaStream_t st = h->stream;
   CK(h->prob.ensure(sizeof(double) * N));
   CK(h->region.ensure(N));

@@ -60,8 +60,9 @@ class ModelBundle:
             if a.shape != shp:
                 raise ParameterError(f"{k} must have shape {shp}, got {a.shape}")
             self.params[k] = a
-        self.feature_mean = np.asarray(self.feature_mean, dtype=float)
-        self.feature_std = np.asarray(self.feature_std, dtype=float)
+        # contiguous copies: the C ABI reads them as raw 33-double arrays
+        self.feature_mean = np.ascontiguousarray(self.feature_mean, dtype=float)
+        self.feature_std = np.ascontiguousarray(self.feature_std, dtype=float)
         if self.feature_mean.shape != (FEATURE_DIM,) or self.feature_std.shape != (FEATURE_DIM,):
             raise ParameterError("feature statistics must be 33-vectors")
         if np.any(self.feature_std <= 0):

@@ -69,7 +69,7 @@ def sharded_full_pseudospectrum(A, grid, group=None, label: str = "matrix"):
     import torch
     from . import core
     dev = torch.device("cuda", torch.cuda.current_device())
-    vals = sharded_sigma(grid.points().ravel(), lambda z: core.smin_many(A, z, label=label),
+    vals = sharded_sigma(grid.points().ravel(), lambda z: core.smin_many(A, z, label=label, device=dev.index),
                          group=group, device=dev)
     return core.SigmaField(grid, vals.reshape(grid.shape))
 
@@ -109,8 +109,8 @@ def sharded_hybrid_pseudospectrum(bundle, A, grid, eps: float, group=None, probe
     region = pipeline.predicted_region(prob, bundle.tau_star)
     t_nn = time.perf_counter() - t0
     t0 = time.perf_counter()
-    vals = sharded_restricted_sigma(grid, region, lambda z: core.smin_many(A, z, label=label), group=group,
-                                    device=dev)
+    vals = sharded_restricted_sigma(grid, region, lambda z: core.smin_many(A, z, label=label, device=dev.index),
+                                    group=group, device=dev)
     t_restricted = time.perf_counter() - t0
     fld = core.SigmaField(grid, vals)
     fld.eps = eps

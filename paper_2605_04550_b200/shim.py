@@ -98,14 +98,11 @@ def install(ps=None, predictor: bool = True):
             _patch(ps, name, fn)
 
     if predictor:
-        cache: dict[int, pipeline.ModelBundle] = {}
-
         @tr
         def _predict_points(bundle, gf, zs):
-            ours = cache.get(id(bundle))
-            if ours is None or ours.tau_star != bundle.tau_star:
-                ours = pipeline.ModelBundle.from_reference(bundle)
-                cache[id(bundle)] = ours
+            # converted on every call (one 59,841-value concatenate): a cache keyed on the bundle's
+            # identity would serve stale weights after the bundle is mutated or its id reused
+            ours = pipeline.ModelBundle.from_reference(bundle)
             return pipeline._predict_points(ours, gf, np.asarray(zs, dtype=complex))
 
         @tr

@@ -122,8 +122,15 @@ class TestValidation:
         A[0, 0] = np.nan
         with pytest.raises(ParameterError):
             core.smin_many(A, [1j])
-        with pytest.raises(ParameterError):
-            core.smin_many(np.eye(3), [np.nan])
+
+    def test_non_finite_shift_is_numerical_error(self):
+        """The reference's svd raises LinAlgError on a NaN shift, reported as NumericalError with
+        the point index and z (core.py:157-166)."""
+        from paper_2605_04550_b200.core import NumericalError
+        with pytest.raises(NumericalError, match="point index 1"):
+            core.smin_many(np.eye(3), [0.5, np.nan, 1j])
+        with pytest.raises(NumericalError):
+            core.smin_at(np.eye(3), complex(np.inf, 0))
 
     def test_too_small(self):
         with pytest.raises(ParameterError):
