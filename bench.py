@@ -1,22 +1,32 @@
 #!/usr/bin/env python3
 """bench.py — throughput of the σ_min(zI - A) grid evaluator (the BASELINE.json metric).
 
-Workload (BASELINE.json configs[1]): Grcar n=400, full 200 x 200 grid over
-[-1,3] x [-3.5,3.5]; one step = one full-grid σ_min sweep (40,000 shifts, every value checked
-by the parity suite against the reference's zgesdd). With N GPUs (torchrun, one rank per GPU)
-the grid is widened to 200 x 200N over the same box and its points are dealt cyclically
-(point p -> rank p mod N): per-GPU work is fixed (weak scaling), and the σ map is gathered to
-rank 0 over NCCL at the end of every step — the only exchange in the path.
+Headline workload (BASELINE.json configs[4], the config the 1/2/4/8-GPU metric is
+quoted on): 64 seeded noisy banded Toeplitz matrices, n=4000, (kl,ku)=(3,3), complex128, a full
+1024 x 1024 grid each. One step = one whole matrix per GPU: rank r evaluates matrix
+(s*N + r) mod 64 at step s, so the steps walk through distinct matrices of the batch. The matrices
+are independent objects, dealt over the ranks with no data-path collective: per-GPU
+work is fixed as N grows ("scaling": "weak"). Each rank keeps the σ maps it computed.
 
-Keys beyond the driver contract (see DESIGN.md §Measurement):
-  roofline      the dominant kernel of the step against its bound: the bisection engine is
-                FP64-bound (peak = DFMA microbenchmark measured in this run, MEASURED_PEAKS.json
-                has no FP64 figure); the Lanczos engine is HBM-bound (peak = MEASURED_PEAKS hbm_gbs)
-  cpu_baseline  the oracle port (numpy zgesdd per shift = the reference's own computation,
-                pseudospec/core.py:141-168) on a bounded sample, 1 thread, rank 0 at N=1 only
-  e2e           the same metric through the public API (full_pseudospectrum / smin_many with
-                host arrays: H2D of the shifts and D2H of the σ map inside the timed region)
---impl reference runs the oracle port on all host cores instead (rank 0 only).
+--config C1..C4 are the single-matrix configs (secondary lines). Their fixed grid is dealt cyclically
+(point p -> rank p mod N, shard.py) and the σ map is all-gathered over NCCL inside every step, the
+path's only exchange ("scaling": "strong").
+
+--gpus N without torchrun re-executes this script under `torch.distributed.run` with N ranks
+(one process per GPU, rendezvous on 127.0.0.1).
+
+Keys beyond the driver contract (DESIGN.md §8):
+  roofline          the dominant kernel of the step (largest CUDA-event window) against its bound;
+                    every window is taken from events recorded on that kernel's own stream, with no
+                    host round trip inside. Bisection/classification: FP64 (peak = DFMA
+                    microbenchmark measured in this run; MEASURED_PEAKS.json has no FP64 figure);
+                    Lanczos: HBM (peak = MEASURED_PEAKS hbm_gbs).
+  lu_solve_model    SURVEY §8(d)'s algorithmic per-z model (LU + k(z) inverse-Lanczos steps, band bytes)
+  cpu_baseline      the oracle port (numpy zgesdd per shift = the reference's computation,
+                    pseudospec/core.py:141-168) on a bounded sample, rank 0 at N=1 only
+  e2e               the same metric through the public API (full_pseudospectrum with host arrays:
+                    band, axes H2D and the σ map D2H inside the timed region)
+--impl reference runs the reference's CPU computation on all host cores instead (rank 0 only).
 """
 
 from __future__ import annotations
@@ -24,6 +34,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
+import socket
 import subprocess
 import sys
 import threading
@@ -37,24 +49,51 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "sigma_min(zI-A) grid points/sec at 1/2/4/8 B200; % of per-z FP64/HBM roofline"
 UNIT = "points/s"
-WORKLOAD = "C2: Grcar n=400 (kl,ku)=(1,3), full 200x200 grid over [-1,3]x[-3.5,3.5], sigma_min at every point"
+WORKLOAD = {
+    "C5": "C5: 64 seeded noisy banded Toeplitz n=4000 (3,3) complex128, full 1024x1024 grid per matrix; "
+          "one step = one whole matrix per GPU, matrix (step*N + rank) mod 64",
+    "C4": "C4: convection-diffusion n=2000 Pe=50 (1,1), fixed 512x512 grid dealt over the GPUs",
+    "C3": "C3: complex banded Toeplitz n=1000 (2,3), fixed 256x256 grid dealt over the GPUs",
+    "C2": "C2: Grcar n=400 (1,3), fixed 200x200 grid over [-1,3]x[-3.5,3.5] dealt over the GPUs",
+    "C1": "C1: Grcar n=100 (1,3), fixed 50x50 grid over [-1,3]x[-3.5,3.5] dealt over the GPUs",
+}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", help="workload (C1..C4); C2 is the headline")
+    ap.add_argument("--config", default="C5", help="workload C1..C5; C5 (BASELINE configs[4]) is the headline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-guided", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--no-e2e", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--dist-selftest", action="store_true", help=argparse.SUPPRESS)
+    return ap.parse_args(argv)
+
+
+# ----------------------------------------------------------------------------- launcher
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N > 1 outside torchrun: run this script as N ranks (one per GPU) on this node."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the communicator log (nranks) for the driver
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -101,71 +140,134 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU legs
+def host_info() -> dict:
+    model = platform.processor() or ""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        info = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if info:
+            blas = f"{info[0].get('internal_api')} {info[0].get('version')}"
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "blas": blas, "numpy": np.__version__}
+
+
+def _dense(cfg, m=0):
+    A = cfg.matrix(m).todense()
+    return A.real.copy() if np.all(A.imag == 0) else A
+
+
 def _oracle_chunk(args):
     A, zs = args
     from oracle.sigma_oracle import smin_restated
     return smin_restated(A, zs)
 
 
-def cpu_oracle_rate(A_dense, zs, cores: int) -> tuple[float, float]:
-    """pts/s of the oracle port (reference computation) over zs with `cores` processes."""
+def _reference_chunk(args):
+    """The reference package's own smin_many (baseline/_ref, stock code path; real A only)."""
+    A, zs = args
+    sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+    from pseudospec import core as rcore
+    return rcore.smin_many(A, zs, chunk=1)
+
+
+def _reference_available() -> bool:
+    return (ROOT / "baseline" / "_ref" / "pseudospec" / "core.py").exists()
+
+
+def cpu_rate(fn, A_dense, zs, procs: int, blas_threads: int) -> tuple[float, float]:
+    """pts/s of `fn` over zs: `procs` processes (each OPENBLAS `blas_threads`) or in-process."""
+    from threadpoolctl import threadpool_limits
     t0 = time.perf_counter()
-    if cores <= 1:
-        _oracle_chunk((A_dense, zs))
+    if procs <= 1:
+        with threadpool_limits(blas_threads):
+            fn((A_dense, zs))
     else:
         from concurrent.futures import ProcessPoolExecutor
-        os.environ["OPENBLAS_NUM_THREADS"] = "1"
-        chunks = np.array_split(zs, cores * 2)
-        with ProcessPoolExecutor(max_workers=cores) as ex:
-            list(ex.map(_oracle_chunk, [(A_dense, c) for c in chunks]))
+        os.environ["OPENBLAS_NUM_THREADS"] = str(blas_threads)
+        chunks = [c for c in np.array_split(zs, procs) if c.size]
+        with ProcessPoolExecutor(max_workers=procs) as ex:
+            list(ex.map(fn, [(A_dense, c) for c in chunks]))
     dt = time.perf_counter() - t0
     return zs.size / dt, dt
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU computation (oracle port) on all host cores."""
+    """--impl reference: the reference's CPU computation of the path on the host cores, rank 0 only.
+    Real A (C1, C2, C4): the reference package's own smin_many from baseline/_ref, one process per core
+    (OPENBLAS_NUM_THREADS=1: SURVEY §0.6's best reference configuration). Complex A (C3, C5): the reference
+    casts A to real (core.py:112-119), so the oracle port (the same zgesdd call without the cast) runs.
+    n=4000 (C5) takes ~75 s per shift on one core, so its step is one shift on all cores' BLAS threads."""
     if rank != 0:
         return
     from paper_2605_04550_b200 import configs
     cfg = configs.CONFIGS[args.config]
-    A = cfg.matrix(0).todense()
-    if not np.iscomplexobj(A) or np.all(A.imag == 0):
-        A = A.real.copy()
+    A = _dense(cfg)
     cores = os.cpu_count() or 1
-    per_step = {"C1": 40, "C2": 12, "C3": 1, "C4": 1}.get(args.config, 4) * cores
+    real = not np.iscomplexobj(A)
+    fn, kind = (_reference_chunk, "reference") if real and _reference_available() else (_oracle_chunk, "port")
+    if args.config == "C5":
+        per_step, procs, blas = 1, 1, cores
+    else:
+        per_step, procs, blas = {"C1": 40, "C2": 4, "C3": 1, "C4": 1}[args.config] * cores, cores, 1
     rng = np.random.default_rng(7)
     pts = cfg.grid.points().ravel()
     for _ in range(args.warmup):
-        cpu_oracle_rate(A, pts[rng.choice(pts.size, max(cores, per_step // 4), replace=False)], cores)
+        cpu_rate(fn, A, pts[rng.choice(pts.size, per_step, replace=False)], procs, blas)
     times, npts = [], 0
     for _ in range(args.steps):
         zs = pts[rng.choice(pts.size, per_step, replace=False)]
-        _, dt = cpu_oracle_rate(A, zs, cores)
+        _, dt = cpu_rate(fn, A, zs, procs, blas)
         times.append(dt)
         npts += zs.size
     value = npts / sum(times)
+    how = (f"{per_step} random grid shift(s) per step of the {args.config} grid, "
+           + ("pseudospec.core.smin_many (baseline/_ref, unmodified)" if kind == "reference"
+              else "numpy zgesdd per shift (oracle port of pseudospec/core.py:141-168, complex A kept)")
+           + (f" in {procs} processes, OPENBLAS_NUM_THREADS=1" if procs > 1 else f", {blas} BLAS threads"))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-        "data": "synthetic (seeded BASELINE config)",
-        "config": {"workload": WORKLOAD if args.config == "C2" else args.config,
-                   "sample_points_per_step": per_step},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{per_step} random grid shifts per step of the {args.config} grid, "
-                                   f"numpy zgesdd per shift (pseudospec/core.py:141-168) in "
-                                   f"{cores} processes, OPENBLAS_NUM_THREADS=1"},
+        "higher_is_better": True, "scaling": "weak" if args.config == "C5" else "strong", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (seeded BASELINE config)",
+        "config": {"workload": WORKLOAD[args.config], "sample_points_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": how, **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_line(cfg, name) -> dict:
+    """The oracle port on a bounded sample (~10-30 s), rank 0 at N=1."""
+    A = _dense(cfg)
+    pts = cfg.grid.points().ravel()
+    rng = np.random.default_rng(11)
+    cores = os.cpu_count() or 1
+    if name == "C5":  # ~75 s per shift on one core: one shift on all cores' BLAS threads
+        ns, threads = 1, cores
+    else:
+        ns, threads = {"C1": 2500, "C2": 200, "C3": 12, "C4": 3}[name], 1
+    zs = pts[rng.choice(pts.size, ns, replace=False)]
+    rate, dt = cpu_rate(_oracle_chunk, A, zs, 1, threads)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{ns} random shift(s) of the {name} grid, numpy zgesdd per shift (the reference's "
+                      f"pseudospec/core.py:141-168 computation), {threads} BLAS thread(s), {dt:.1f} s",
+            **host_info()}
 
 
 # ----------------------------------------------------------------------------- our arm
 def run_guided(cfg, grid, args) -> dict:
     """BASELINE C2's MLP-guided run (pipeline.py:273-297): hierarchical prediction (K2) with the bundle
     the reference trained and calibrated (tests/golden/model_grcar.npz), 5x5-dilated region, restricted
-    σ sweep (K1). Reports the reference's own timing split (t_nn incl. the host O(n^3) global_features,
-    t_restricted) and its metrics against the full map (pipeline.py:300-331)."""
+    σ sweep (K1). Reports the reference's own timing split and its metrics against the full map."""
     import torch
 
     from paper_2605_04550_b200 import core, pipeline
@@ -180,9 +282,6 @@ def run_guided(cfg, grid, args) -> dict:
         if it >= args.warmup:
             t_nn.append(res.t_nn)
             t_r.append(res.t_restricted)
-    gf_t = time.perf_counter()
-    pipeline.global_features(A)
-    gf_t = time.perf_counter() - gf_t
     full = core.full_pseudospectrum(cfg.matrix(0), grid)
     truth = full.values <= eps
     region = res.region
@@ -193,11 +292,34 @@ def run_guided(cfg, grid, args) -> dict:
     same = bool(np.array_equal(res.field.values[region], full.values[region]))
     tn, tr = float(np.median(t_nn)), float(np.median(t_r))
     return {"eps": eps, "tau_star": bundle.tau_star, "nn_evaluations": int(res.nn_evaluations),
-            "grid_fraction": float(region.mean()), "t_nn_s": tn, "t_global_features_host_s": gf_t,
-            "t_restricted_s": tr, "t_hybrid_s": tn + tr,
+            "grid_fraction": float(region.mean()), "t_nn_s": tn, "t_restricted_s": tr, "t_hybrid_s": tn + tr,
             "grid_points_per_s": grid.size / (tn + tr), "recall": recall, "coverage": coverage,
             "restricted_equals_full_bitwise": same,
-            "note": "t_nn includes the host O(n^3) global_features (eig/svd, SURVEY 8f row 1)"}
+            "note": "t_nn includes global_features (host eig/svd, cached per matrix after the first call)"}
+
+
+def lu_solve_model(n, kl, ku, s, fp64_tf, hbm_gbs) -> dict:
+    """F(z) = F_LU + k(z) F_it, F_LU = n p (8(p+q)+6), F_pair = n (8p + 8(p+q) + 6),
+    F_it = 2 F_pair + 40 n, B_band = 16 n (2p+q+1); t_roof(z) = max(F/P_FP64, B_band/BW). k(z) is recorded by
+    K1 for the engine-L points (mean k below); engine-B points carry no Lanczos count, so the model is
+    evaluated over engine-L points, where the kernel runs exactly this algorithm."""
+    p, q = kl, ku
+    f_lu = n * p * (8 * (p + q) + 6)
+    f_it = 2 * n * (8 * p + 8 * (p + q) + 6) + 40 * n
+    b_band = 16 * n * (2 * p + q + 1)
+    kbar = s["lanczos_iters"] / s["n_lanczos"] if s["n_lanczos"] else 0.0
+    f = f_lu + kbar * f_it
+    t = max(f / (fp64_tf * 1e12), b_band / (hbm_gbs * 1e9))
+    return {"F_LU": f_lu, "F_it": f_it, "B_band": b_band, "k_mean_engine_L": kbar, "flops_per_point": f,
+            "bound": "fp64" if f / (fp64_tf * 1e12) >= b_band / (hbm_gbs * 1e9) else "hbm",
+            "roof_points_per_s_per_gpu": 1.0 / t}
+
+
+def _sum_stats(stats: list[dict]) -> dict:
+    keys = ["n_points", "n_lanczos", "n_bisect", "lanczos_iters", "pd_tests", "flops_bisect", "flops_lanczos",
+            "bytes_lanczos", "ms_bisect", "ms_lanczos", "ms_total", "ms_classify", "flops_classify", "ms_fallback",
+            "launches"]
+    return {k: sum(s[k] for s in stats) for k in keys}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -206,27 +328,48 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2605_04550_b200 import _lib, configs, core
+    from paper_2605_04550_b200 import _lib, configs, core, shard
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     h = _lib.handle(local_rank)
-    cfg = configs.CONFIGS[args.config]
-    A = cfg.matrix(0)
-    g0 = cfg.grid
-    grid = core.make_grid(g0.x_min, g0.x_max, g0.y_min, g0.y_max, g0.nx * world, g0.ny)
+    name = args.config
+    cfg = configs.CONFIGS[name]
+    grid = cfg.grid
+    batch = cfg.batch > 1
     pts = grid.points().ravel()
-    mine = np.ascontiguousarray(pts[rank::world])
+    if batch:  # whole matrices per rank: every rank evaluates the full grid of its own matrix
+        mine = pts
+        mats = {}
+
+        def matrix_of(step):
+            m = (step * world + rank) % cfg.batch
+            if m not in mats:
+                mats[m] = cfg.matrix(m)
+            return m, mats[m]
+    else:
+        mine = np.ascontiguousarray(pts[rank::world])
+        A0 = cfg.matrix(0)
+
+        def matrix_of(step):
+            return 0, A0
     P = mine.size
-    with h.lock:
-        core._set_matrix(h, A)
-    d_zs = torch.from_numpy(mine.view(np.float64).copy()).to(dev)
+    d_zs = torch.from_numpy(np.ascontiguousarray(mine).view(np.float64).copy()).to(dev)
     d_out = torch.empty(P, dtype=torch.float64, device=dev)
     d_iters = torch.empty(P, dtype=torch.int32, device=dev)
     d_status = torch.empty(P, dtype=torch.int8, device=dev)
-    gathered = torch.empty(world * P, dtype=torch.float64, device=dev) if world > 1 else None
+    m_pad = (pts.size + world - 1) // world
+    gather_in = torch.full((m_pad,), float("nan"), dtype=torch.float64, device=dev) if (world > 1 and not batch) else None
+    gathered = torch.empty(world * m_pad, dtype=torch.float64, device=dev) if gather_in is not None else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    used = []
+
+    def prepare(step):  # outside the timed region: the step's matrix resident on the device
+        m, A = matrix_of(step)
+        with h.lock:
+            core._set_matrix(h, A)
+        used.append(m)
 
     def step():
         rc = h.lib.psb_smin_points_device(h.h, C.c_void_p(d_zs.data_ptr()), P, None,
@@ -234,8 +377,9 @@ def run_ours(args, rank, world, local_rank):
                                           C.c_void_p(d_status.data_ptr()), C.c_void_p(stream.cuda_stream))
         if rc != 0:
             raise RuntimeError(f"psb_smin_points_device failed: {h.error()}")
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, d_out)
+        if gathered is not None:  # the path's one exchange: the σ map all-gathered over NCCL
+            gather_in[:P].copy_(d_out)
+            dist.all_gather_into_tensor(gathered, gather_in)
 
     def barrier():
         if world > 1:
@@ -244,19 +388,23 @@ def run_ours(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)  # covers warm-up, the timed steps and the e2e leg
     sampler.start()
     time.sleep(0.3)
+    s_idx = 0
     for _ in range(max(args.warmup, 0)):
+        prepare(s_idx)
         step()
+        s_idx += 1
     torch.cuda.synchronize()
-    # correctness guard on the timed configuration: every point converged
     st = d_status.cpu().numpy()
     assert (st <= 2).all(), "non-converged points in the benchmark step"
 
-    stats = []
-    step_ms = []
+    stats, step_ms = [], []
     barrier()
     torch.cuda.synchronize()
     for _ in range(args.steps):
+        prepare(s_idx)
+        s_idx += 1
         flush.random_(0, 255)  # evict L2 (256 MiB > 126 MB) between timed steps, outside the events
+        barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -265,41 +413,52 @@ def run_ours(args, rank, world, local_rank):
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
         stats.append(h.stats())
+        assert (d_status.cpu().numpy() <= 2).all(), "non-converged points in a timed step"
     torch.cuda.synchronize()
     barrier()
 
-    ms_local = float(np.mean(step_ms))
-    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    # max over ranks of the summed step time (each rank runs the same number of steps)
+    t = torch.tensor([float(np.sum(step_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    value = world * P / (ms * 1e-3)
+    ms = float(t.item()) / args.steps
+    units = world * P if batch else pts.size  # points every rank together finishes per step
+    value = units / (ms * 1e-3)
 
     # ---- e2e through the public API, host buffers, copies inside the timed region
-    e2e_ms = []
-    for it in range(args.warmup + args.steps):
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        if world == 1:
-            fld = core.full_pseudospectrum(A, grid)
+    e2e_ms, h2d, d2h = [], 0, 0
+    if not args.no_e2e:
+        for it in range(args.warmup + min(args.steps, 3 if batch else args.steps)):
+            m, A = matrix_of(s_idx)
+            s_idx += 1
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            if batch or world == 1:
+                fld = core.full_pseudospectrum(A, grid, device=local_rank)
+            else:
+                fld = shard.sharded_full_pseudospectrum(A, grid)
+            torch.cuda.synchronize()
+            dt = (time.perf_counter() - t0) * 1e3
+            if it >= args.warmup:
+                e2e_ms.append(dt)
+            band_bytes = A.band.size * 16
+        if batch or world == 1:
+            h2d = band_bytes + (grid.nx + grid.ny) * 8
+            d2h = grid.size * 9  # σ (f64) + status (i8)
         else:
-            out = core.smin_many(A, mine)
-        torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) * 1e3
-        if it >= args.warmup:
-            e2e_ms.append(dt)
+            h2d = band_bytes + P * 16 + m_pad * 8  # band, this rank's shifts, its padded shard for the gather
+            d2h = P * (8 + 4 + 1) + world * m_pad * 8  # its σ / iters / status, the gathered map
     clocks = sampler.stop()
-    te = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * P / (float(te.item()) * 1e-3)
-    # grid path: the two axes (shifts are formed on the device); sharded path: this rank's shifts
-    h2d = (grid.nx + grid.ny) * 8 if world == 1 else P * 16
-    d2h = (grid.size * 9) if world == 1 else P * 9       # sigma (f64) + status (i8)
+    e2e_value = None
+    if e2e_ms:
+        te = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_value = units / (float(te.item()) * 1e-3)
 
-    # ---- roofline of the dominant kernel
-    s = stats[-1]
+    # ---- roofline of the dominant kernel (largest CUDA-event window of the step)
+    S = _sum_stats(stats)
     fp64_peak = h.fp64_peak()
     hbm_peak = 6455.9
     mp = ROOT / "MEASURED_PEAKS.json"
@@ -308,68 +467,79 @@ def run_ours(args, rank, world, local_rank):
             hbm_peak = float(json.loads(mp.read_text())["hbm_gbs"])
         except Exception:
             pass
-    kern = {
-        "bisect": {"bound": "fp64", "achieved": s["flops_bisect"] / (s["ms_bisect"] * 1e-3) / 1e12,
-                   "peak": fp64_peak, "unit": "TFLOP/s", "ms": s["ms_bisect"]},
-        "lanczos": {"bound": "hbm", "achieved": s["bytes_lanczos"] / (s["ms_lanczos"] * 1e-3) / 1e9
-                    if s["ms_lanczos"] > 0 else 0.0, "peak": hbm_peak, "unit": "GB/s", "ms": s["ms_lanczos"]},
+    K = args.steps
+
+    def kern(bound, work, ms_sum, kname):
+        ms_k = ms_sum / K
+        if bound == "fp64":
+            ach = work / (ms_sum * 1e-3) / 1e12 if ms_sum > 0 else 0.0
+            d = {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s"}
+        else:
+            ach = work / (ms_sum * 1e-3) / 1e9 if ms_sum > 0 else 0.0
+            d = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s"}
+        d.update({"frac": ach / d["peak"], "ms": ms_k, "kernel": kname,
+                  "work_per_launch": work / K})
+        return d
+
+    kerns = {
+        "bisect": kern("fp64", S["flops_bisect"], S["ms_bisect"], "k_bisect (engine B, mode 1)"),
+        "lanczos": kern("hbm", S["bytes_lanczos"], S["ms_lanczos"], "k_lanczos (engine L)"),
+        "classify": kern("fp64", S["flops_classify"], S["ms_classify"], "k_bisect (mode 0, classification)"),
     }
-    for v in kern.values():
-        v["frac"] = v["achieved"] / v["peak"] if v["peak"] else None
-    dom = "bisect" if s["ms_bisect"] >= s["ms_lanczos"] else "lanczos"
+    dom = max(kerns, key=lambda k: kerns[k]["ms"])
+    roof = dict(kerns[dom])
+    ms_local = float(np.mean(step_ms))
+    assert roof["ms"] <= ms_local * 1.001 + 1e-3, f"kernel window {roof['ms']} ms > step {ms_local} ms"
+    roof["share_of_step"] = roof["ms"] / ms_local
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(args.config, {}).get(dom)
+            traffic = json.loads(tf.read_text()).get(name, {}).get(dom)
         except Exception:
             traffic = None
-    roof = dict(kern[dom])
-    roof["kernel"] = f"k_{dom}"
     roof["traffic"] = traffic
-    # per-z FP64 roofline of the whole step (north star): G*P_FP64 / mean flops per point
-    flops_pt = (s["flops_bisect"] + s["flops_lanczos"]) / max(1, s["n_points"])
+    n_, kl_, ku_ = (cfg.matrix(0).n, cfg.matrix(0).kl, cfg.matrix(0).ku)
+    flops_pt = (S["flops_bisect"] + S["flops_lanczos"] + S["flops_classify"]) / max(1, S["n_points"])
     roof_pts = fp64_peak * 1e12 / flops_pt if flops_pt > 0 else None
+    model = lu_solve_model(n_, kl_, ku_, S, fp64_peak, hbm_peak)
 
     guided = None
-    if rank == 0 and world == 1 and args.config in ("C1", "C2") and not args.no_guided:
+    if rank == 0 and world == 1 and name in ("C1", "C2") and not args.no_guided:
         guided = run_guided(cfg, grid, args)
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        Ad = A.todense()
-        Ad = Ad.real.copy() if np.all(Ad.imag == 0) else Ad
-        rng = np.random.default_rng(11)
-        ns = {"C1": 2500, "C2": 200, "C3": 12, "C4": 3}.get(args.config, 8)
-        zs = pts[rng.choice(pts.size, ns, replace=False)]
-        rate, dt = cpu_oracle_rate(Ad, zs, 1)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{ns} random shifts of the {args.config} grid, numpy zgesdd per shift "
-                         f"(the reference's pseudospec/core.py:141-168 computation), 1 thread, {dt:.1f} s"}
+        cpu = cpu_baseline_line(cfg, name)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded BASELINE config, no dataset)",
-            "config": {"workload": WORKLOAD if args.config == "C2" else cfg.description,
-                       "grid": f"{grid.ny}x{grid.nx}", "points_per_gpu": P, "points_total": world * P,
-                       "sharding": "cyclic point p -> rank p mod N; sigma map all-gathered over NCCL each step",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if batch else "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded BASELINE config, no dataset)",
+            "config": {"workload": WORKLOAD[name], "grid": f"{grid.ny}x{grid.nx}", "points_per_gpu": P,
+                       "points_per_step": units,
+                       "matrices_timed_rank0": used[args.warmup:args.warmup + args.steps] if batch else [0],
+                       "sharding": ("matrices dealt over ranks (matrix (step*N + rank) mod 64), no collective"
+                                    if batch else "cyclic point p -> rank p mod N; sigma map all-gathered over "
+                                                  "NCCL inside every step"),
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"dp{world}"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "core.full_pseudospectrum" if world == 1 else "core.smin_many (rank shard)"},
             "roofline": roof,
-            "roofline_kernels": kern,
-            "per_z_fp64_roofline": {"points_per_s": roof_pts * world if roof_pts else None,
-                                    "frac": value / (roof_pts * world) if roof_pts else None,
-                                    "flops_per_point": flops_pt},
-            "engines": {"lanczos_points": s["n_lanczos"], "bisect_points": s["n_bisect"],
-                        "lanczos_steps": s["lanczos_iters"], "pd_tests": s["pd_tests"]},
-            # per step: the classification kernel, then engine L and engine B when they have points
-            "gpu_launches": int(sum(1 + (s_["grid_lanczos"] > 0) + (s_["grid_bisect"] > 0) for s_ in stats)),
+            "roofline_kernels": kerns,
+            "per_z_fp64_roofline": {"executed_flops_per_point": flops_pt,
+                                    "points_per_s": roof_pts * world if roof_pts else None,
+                                    "frac": value / (roof_pts * world) if roof_pts else None},
+            "lu_solve_model": model,
+            "engines": {"lanczos_points": S["n_lanczos"] // K, "bisect_points": S["n_bisect"] // K,
+                        "lanczos_steps": S["lanczos_iters"] // K, "pd_tests": S["pd_tests"] // K},
+            "gpu_launches": int(S["launches"]),
             "clocks": clocks,
         }
+        if e2e_value is not None:
+            line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                           "api": ("core.full_pseudospectrum (one matrix per rank)" if batch or world == 1
+                                   else "shard.sharded_full_pseudospectrum")}
         if cpu:
             line["cpu_baseline"] = cpu
         if guided:
@@ -377,24 +547,52 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- launcher self-test
+def run_dist_selftest(rank, world):
+    """CPU check of the multi-rank plumbing (gloo): cyclic deal, all-gather, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_04550_b200 import configs, shard
+    grid = configs.CONFIGS["C1"].grid
+    zs = grid.points().ravel()
+    vals = shard.sharded_sigma(zs, lambda z: np.abs(z) + rank * 0.0)
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"selftest": True, "world": world, "max_over_ranks": float(t.item()),
+                          "gather_ok": bool(np.array_equal(vals, np.abs(zs)))}), flush=True)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"[bench] note: WORLD_SIZE={world} ranks, --gpus {args.gpus}; reporting n_gpus={world}",
+              file=sys.stderr)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    import torch
+    import torch.distributed as dist
+    if args.dist_selftest:
+        dist.init_process_group("gloo")
+        try:
+            run_dist_selftest(rank, world)
+        finally:
+            dist.destroy_process_group()
+        return
     if world > 1:
-        import torch
-        import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
-            import torch.distributed as dist
             dist.destroy_process_group()
 
 

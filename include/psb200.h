@@ -64,13 +64,19 @@ typedef struct {
   int64_t n_bisect;       /* points finished by the bisection engine */
   int64_t lanczos_iters;  /* total Lanczos steps */
   int64_t pd_tests;       /* total LDL^H positive-definiteness tests (incl. classification) */
-  double flops_bisect;    /* algorithmic FP64 flops executed by the bisection engine */
-  double flops_lanczos;   /* algorithmic FP64 flops executed by the Lanczos engine (LU + steps) */
+  double flops_bisect;    /* FP64 flops executed by the bisection engine's launches (classification excluded) */
+  double flops_lanczos;   /* FP64 flops executed by the Lanczos engine (LU + steps) */
   double bytes_lanczos;   /* algorithmic HBM bytes moved by the Lanczos engine */
-  double ms_bisect;       /* CUDA-event time of the bisection kernel */
-  double ms_lanczos;      /* CUDA-event time of the Lanczos kernel */
-  double ms_total;        /* CUDA-event time of the whole device pipeline */
+  double ms_bisect;       /* CUDA-event window of the bisection engine: its first launch's start to its last
+                             launch's end (the two launches share one work counter) */
+  double ms_lanczos;      /* CUDA-event window of the Lanczos kernel */
+  double ms_total;        /* CUDA-event time of the whole device pipeline (incl. the list-size read-back) */
   int32_t grid_bisect, grid_lanczos; /* CTAs launched */
+  double ms_classify;     /* CUDA-event time of the classification kernel */
+  double flops_classify;  /* FP64 flops of the classification kernel (one LDL^H test per point) */
+  double ms_fallback;     /* CUDA-event time of the fallback bisection launch (0 when not launched) */
+  int32_t launches;       /* kernels launched by the last call (grid shifts, classification, engines, fallback) */
+  int32_t reserved;
 } psb_stats;
 
 int psb_create(int device, psb_handle** out);

@@ -290,7 +290,7 @@ def gen_calib():
     print("calib: passed", rep.passed, rep.tau_star, flush=True)
 
 
-def gen_c5_strat(maps_path="gpurun_out/c5_maps.npz", per_matrix=64, procs=7):
+def gen_c5_strat(maps_path="gpurun_out/c5_maps.npz", per_matrix=64, procs=6):
     """C5 parity pinned on meaningful points: for each of 4 matrices, 64 grid shifts stratified by what
     they exercise, with sigma from the restated zgesdd oracle (complex A). Strata (per matrix):
       24  bisection-engine points with sigma >= the parity floor 1e-5 ||A||_2 (the general-band kernel)
@@ -340,8 +340,65 @@ def gen_c5_strat(maps_path="gpurun_out/c5_maps.npz", per_matrix=64, procs=7):
                             tau=np.array(1e-3))
 
 
+def _random_bundle(ps, seed, tau):
+    rng = np.random.default_rng(seed)
+    params = ps.ModelParams(**{k: rng.standard_normal(s) * 0.1 for k, s in ps.network.PARAM_SHAPES.items()})
+    return ps.ModelBundle(params=params, feature_mean=np.zeros(33), feature_std=np.ones(33), tau_star=tau)
+
+
+def gen_pipeline():
+    """Reference-made fixtures for the shim-level GPU tests, so they also run where the reference package
+    is absent (the GPU box):
+      shim_pipeline.npz  the reference's benchmark() / hybrid_pseudospectrum() / full_pseudospectrum() on
+                         3 generated n=24 matrices, 40x40 grid, eps 0.05, a seeded random bundle (tau 0.3)
+      dataset_labels.npz the reference's build_dataset() (its largest sigma consumer, pipeline.py:128-166)
+                         on 4 generated n=32 matrices, 36x36 grid, eps 0.05, seed 5
+    The inputs (matrices, probe seeds, bundle parameters) are stored with the outputs."""
+    import pseudospec as ps
+    from pseudospec import pipeline as rpl
+    corpus = ps.generate_corpus(ps.GenSpec(n=24, seed=11), 3)
+    grid = ps.make_grid(-4, 4, -4, 4, 40, 40)
+    bundle = _random_bundle(ps, 0, 0.3)
+    out = {"grid": np.array([-4, 4, -4, 4, 40, 40.0]), "eps": np.array(0.05), "tau_star": np.array(0.3)}
+    for k in ps.network.PARAM_SHAPES:
+        out[f"p_{k}"] = np.asarray(getattr(bundle.params, k))
+    with threadpool_limits(1):
+        records, base = rpl.benchmark(bundle, corpus, grid, eps=0.05, baseline=True)
+        for i, e in enumerate(corpus):
+            out[f"matrix_{i}"] = e.matrix
+            out[f"probe_seed_{i}"] = np.array(e.probe_seed)
+            out[f"full_{i}"] = ps.core.full_pseudospectrum(e.matrix, grid).values
+            res = rpl.hybrid_pseudospectrum(bundle, e.matrix, grid, eps=0.05, probe_seed=e.probe_seed)
+            out[f"region_{i}"] = res.region
+            out[f"prob_{i}"] = res.prob_field
+            out[f"hybrid_{i}"] = res.field.values
+            out[f"n_evals_{i}"] = np.array(res.nn_evaluations)
+            m = records[i].metrics
+            out[f"metrics_{i}"] = np.array([m.accuracy, m.precision, m.recall, m.coverage, m.grid_fraction,
+                                            m.tp, m.fp, m.fn], dtype=float)
+            out[f"mae_{i}"] = np.array(records[i].mae_log10_smin)
+    out["count"] = np.array(len(corpus))
+    np.savez_compressed(GOLD / "shim_pipeline.npz", **out)
+    print("shim_pipeline: mae", [float(r.mae_log10_smin) for r in records], flush=True)
+
+    corpus = ps.generate_corpus(ps.GenSpec(n=32, seed=21), 4)
+    grid = ps.make_grid(-4, 4, -4, 4, 36, 36)
+    with threadpool_limits(1):
+        ds = rpl.build_dataset(corpus, grid, eps=0.05, seed=5)
+    out = {"grid": np.array([-4, 4, -4, 4, 36, 36.0]), "eps": np.array(0.05), "count": np.array(len(corpus)),
+           "xy": ds.xy, "features": ds.features, "labels": ds.labels, "matrix_ids": ds.matrix_ids}
+    for i, e in enumerate(corpus):
+        out[f"matrix_{i}"] = e.matrix
+        out[f"index_{i}"] = np.array(e.index)
+        out[f"probe_seed_{i}"] = np.array(e.probe_seed)
+    np.savez_compressed(GOLD / "dataset_labels.npz", **out)
+    print("dataset_labels:", ds.labels.size, "samples,", int(ds.labels.sum()), "positive", flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what == "pipeline":
+        gen_pipeline()
     if what in ("sigma", "all"):
         gen_sigma()
     if what == "small":

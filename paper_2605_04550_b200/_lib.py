@@ -45,7 +45,9 @@ class Stats(C.Structure):
                 ("flops_bisect", C.c_double), ("flops_lanczos", C.c_double),
                 ("bytes_lanczos", C.c_double), ("ms_bisect", C.c_double),
                 ("ms_lanczos", C.c_double), ("ms_total", C.c_double),
-                ("grid_bisect", C.c_int32), ("grid_lanczos", C.c_int32)]
+                ("grid_bisect", C.c_int32), ("grid_lanczos", C.c_int32),
+                ("ms_classify", C.c_double), ("flops_classify", C.c_double), ("ms_fallback", C.c_double),
+                ("launches", C.c_int32), ("reserved", C.c_int32)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -64,7 +64,7 @@ struct psb_handle {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr, stream2 = nullptr;
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[14] = {};  // per-launch timing events (run_pipeline)
   std::string err;
   std::mutex mu;
   // matrix
@@ -88,7 +88,7 @@ struct psb_handle {
   struct LanEntry { const void* f; int lsmem, occ, regs; };
   std::vector<LanEntry> lan_cache;  // engine-L occupancy and registers per kernel
   bool have_matrix = false;
-  DevBuf Ab, AHA, v1, offmin, gbuf, listF;
+  DevBuf Ab, AHA, RT, v1, offmin, gbuf, listF;
   // per call
   DevBuf zs, outidx, out, iters, status, listA, listB, counters, scratch, pivs, dynL, dynD;
   DevBuf xs, ys, prof;
@@ -198,7 +198,7 @@ int psb_create(int device, psb_handle** out) {
 void psb_destroy(psb_handle* h) {
   if (!h) return;
   DeviceGuard dg(h->device);
-  DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->v1, &h->offmin, &h->gbuf, &h->listF, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
+  DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->RT, &h->v1, &h->offmin, &h->gbuf, &h->listF, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
                     &h->counters, &h->scratch, &h->pivs, &h->dynL, &h->dynD, &h->xs, &h->ys, &h->params,
                     &h->feat, &h->eig, &h->prob, &h->region, &h->idx};
   for (DevBuf* b : bufs) b->release();
@@ -310,6 +310,18 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
     h->anorm = std::sqrt(*std::max_element(colsum.begin(), colsum.end()) * *std::max_element(rowsum.begin(), rowsum.end()));
     CK(h->AHA.ensure(sizeof(cd) * (b + 1) * n));
     CK(cudaMemcpy(h->AHA.p, aha.data(), sizeof(cd) * (b + 1) * n, cudaMemcpyHostToDevice));
+    // the same coefficients row-packed for the general-band bisection kernels (BisRow, psb_engines.cuh):
+    // row i = [AHA_d (d = 0..b) | A[i, i-d] (d = 0..kl) | A[i-d, i] (d = 1..ku)]
+    const int RW = 2 * b + 2;
+    std::vector<cd> rt((size_t)RW * n, cd(0, 0));
+    for (int i = 0; i < n; i++) {
+      cd* row = rt.data() + (size_t)i * RW;
+      for (int d = 0; d <= b; d++) row[d] = aha[(size_t)d * n + i];
+      for (int d = 0; d <= kl; d++) row[b + 1 + d] = A[(int64_t)(kl - d) * n + i];
+      for (int d = 1; d <= ku; d++) row[b + 1 + kl + d] = (i - d >= 0) ? A[(int64_t)(kl + d) * n + (i - d)] : cd(0, 0);
+    }
+    CK(h->RT.ensure(sizeof(cd) * rt.size()));
+    CK(cudaMemcpy(h->RT.p, rt.data(), sizeof(cd) * rt.size(), cudaMemcpyHostToDevice));
   }
   // Lanczos start vector: fixed, identical for every z (determinism)
   std::vector<cd> v1(n);
@@ -372,6 +384,9 @@ static double flops_ldl_row(int kl, int ku) { const double b = kl + ku; return 4
 // (8 flops each) -> 4 (b+1)(b+2) + 2 (the two diagonals of M); shared by the probes of a round, and
 // formed once per round for the interior rows of a diagonal-constant band.
 static double flops_g_row(int kl, int ku) { const double b = kl + ku; return 4.0 * (b + 1) * (b + 2) + 2.0; }
+// Forming one G row from the A^H A expansion (g_entry_aha): kl + 1 entries take - conj(z) A[j, j-d] and
+// ku + 1 take - z conj(A[j-d, j]) (one complex FMA, 8 flops, each), plus |z|^2 - lambda on the diagonal.
+static double flops_g_row_aha(int kl, int ku) { return 8.0 * (kl + 1) + 8.0 * (ku + 1) + 2.0; }
 static double flops_lu_row(int kl, int ku) { const int W = kl + ku; return 6.0 * W + 6.0 + kl * (6.0 + 8.0 * W); }
 static double flops_it_row(int kl, int ku) {
   const int W = kl + ku;
@@ -411,7 +426,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   h->stats.n_points = P;
   if (P == 0) return PSB_OK;
 
-  CK(h->counters.ensure(sizeof(unsigned long long) * 24));
+  CK(h->counters.ensure(sizeof(unsigned long long) * 24));  // [16..19]: row counters (classify, B, fallback, B2)
   CK(h->listA.ensure(sizeof(int64_t) * P));
   CK(h->listB.ensure(sizeof(int64_t) * P));
   CK(h->listF.ensure(sizeof(int64_t) * P));
@@ -419,8 +434,11 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 24, st));
 
   // ---- classification: one LDL^H test per point at lambda = (tau S)^2 splits the points
+  // general-band static kernels stage their G-row coefficients per warp in dynamic shared memory
+  const int bsw = (!dyn && !(h->tz_j0 <= h->tz_j1 && h->k_toeplitz)) ? kp.bsmem : 0;
+  auto bsm = [&](int tpb) { return (size_t)(tpb / 32) * (size_t)bsw; };
   int occB = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, kp.b, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occB, kp.b, 128, bsm(128)));
   occB = std::max(occB, 1);
   BisArgs ba;
   ba.n = n; ba.kl = kl; ba.ku = ku;
@@ -432,12 +450,15 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.out = d_out; ba.iters = d_iters; ba.status = d_status;
   ba.listA = h->listA.as<int64_t>(); ba.listB = h->listB.as<int64_t>(); ba.counters = cnt;
   ba.dyn_L = nullptr; ba.dyn_D = nullptr;
+  ba.RT = h->RT.as<double2>();
+  ba.rowctr = cnt + 16;  // classification rows x probes
   ba.mode = 0; ba.fallback = 0; ba.rmin2 = 0.0;
   ba.secant = h->k_secant ? 1 : 0;
   ba.tz_j0 = h->k_toeplitz ? h->tz_j0 : 1;
   ba.tz_j1 = h->k_toeplitz ? h->tz_j1 : 0;
   const int64_t gridC = std::max<int64_t>(1, std::min<int64_t>((int64_t)occB * h->num_sms, (P + 127) / 128));
   int64_t gridB = (int64_t)occB * h->num_sms, gridB2 = 0;
+  bool b2pair = false;  // the expansion launch runs the pair variant (one probe per lane)
   if (dyn) {
     const int b = std::max(kl + ku, 1);
     const int64_t threads = std::max(gridB, gridC) * 128;
@@ -455,7 +476,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   }
   ba.gb_T = gridC * 128;
   CK(cudaEventRecord(h->ev[0], st));
-  kp.b<<<(unsigned)gridC, 128, 0, st>>>(ba);
+  kp.b<<<(unsigned)gridC, 128, bsm(128), st>>>(ba);
   CK(cudaGetLastError());
   CK(cudaEventRecord(h->ev[1], st));
   // One host round trip reads the list lengths: it sizes both grids and, more importantly, makes the
@@ -520,6 +541,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     }
     CK(cudaEventRecord(h->ev[5], st));
     CK(cudaStreamWaitEvent(h->stream2, h->ev[5], 0));
+    CK(cudaEventRecord(h->ev[7], h->stream2));
     kp.l<<<(unsigned)gridL, 32 * kLWarpsPerBlock, lsmem, h->stream2>>>(la);
     CK(cudaGetLastError());
     CK(cudaEventRecord(h->ev[3], h->stream2));
@@ -554,7 +576,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
       for (int cand : {128, 64, 32}) {
         if (h->k_btpb > 0 && cand != h->k_btpb) continue;
         int occM = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, f, cand, 0);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occM, f, cand, bsm(cand));
         if (e != cudaSuccess) return e;
         occM = std::max(occM, 1);
         int occ = occM;
@@ -601,12 +623,13 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
         const int used = ((wB1 + 3) / 4) * fw.wregs;                                  // per 16K slice
         const int per_slice = std::max(0, (16384 - used) / fp.wregs);
         const int64_t ex2 = std::min<int64_t>((int64_t)4 * per_slice * h->num_sms, (2 * nB + 31) / 32);
-        if (ex2 > 0) { gridB2 = ex2; fB2 = kp.bm2; tpb2 = 32; g2 = 2; }
+        if (ex2 > 0) { gridB2 = ex2; fB2 = kp.bm2; tpb2 = 32; g2 = 2; b2pair = true; }
       }
     }
     (void)g2;
     ba.mode = 1;
     ba.max_tests = 200;
+    ba.rowctr = cnt + 17;  // engine-B rows x probes (the expansion launch counts into cnt[19])
     ba.gb_T = gridB * tpbB + gridB2 * tpb2;
     ba.tid_base = 0;
     if (tzk) {  // after the host round trip the classification kernel is done: resizing is safe
@@ -618,12 +641,14 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
       CK(h->dynD.ensure(sizeof(double) * (size_t)ba.gb_T * 2 * std::max(kl + ku, 1)));
       ba.dyn_L = h->dynL.as<double2>(); ba.dyn_D = h->dynD.as<double>();
     }
-    kp.bm<<<(unsigned)gridB, tpbB, 0, st>>>(ba);
+    CK(cudaEventRecord(h->ev[8], st));
+    kp.bm<<<(unsigned)gridB, tpbB, bsm(tpbB), st>>>(ba);
     CK(cudaGetLastError());
     if (gridB2 > 0) {
       BisArgs b2 = ba;
       b2.tid_base = gridB * tpbB;
-      fB2<<<(unsigned)gridB2, tpb2, 0, h->stream2>>>(b2);
+      b2.rowctr = cnt + 19;
+      fB2<<<(unsigned)gridB2, tpb2, bsm(tpb2), h->stream2>>>(b2);
       CK(cudaGetLastError());
       CK(cudaEventRecord(h->ev[6], h->stream2));
     }
@@ -634,9 +659,10 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   if (nA > 0) CK(cudaStreamWaitEvent(st, h->ev[3], 0));
   if (gridB2 > 0) CK(cudaStreamWaitEvent(st, h->ev[6], 0));
   CK(cudaEventRecord(h->ev[4], st));
-  unsigned long long hc[16];
+  unsigned long long hc[24];
   CK(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  bool ran_fallback = false;
   if (hc[8] > 0 && opt.force_engine == 0 && !fallback_off(h)) {
     // Engine L points that hit kmax (a tight cluster at sigma_min; tools/fuzz_parity.py) get one more
     // chance on engine B from the bracket [0, lambda_tau]; its answer replaces engine L's only where the
@@ -647,6 +673,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     bf.mode = 1; bf.fallback = 1; bf.rmin2 = 16e-8; bf.max_tests = 200;
     bf.listB = h->listF.as<int64_t>();
     bf.counters = cF;
+    bf.rowctr = cnt + 18;
     CK(cudaMemsetAsync(cF, 0, sizeof(unsigned long long) * 7, st));
     CK(cudaMemcpyAsync(cF + 7, cnt + 8, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
     const int tpbF = 128;
@@ -661,17 +688,27 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
       CK(h->dynD.ensure(sizeof(double) * (size_t)bf.gb_T * 2 * std::max(kl + ku, 1)));
       bf.dyn_L = h->dynL.as<double2>(); bf.dyn_D = h->dynD.as<double>();
     }
-    kp.bm<<<(unsigned)gridF, tpbF, 0, st>>>(bf);
+    CK(cudaEventRecord(h->ev[9], st));
+    kp.bm<<<(unsigned)gridF, tpbF, bsm(tpbF), st>>>(bf);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(h->ev[10], st));
     CK(cudaStreamSynchronize(st));
+    ran_fallback = true;
   }
   const int64_t nA_run = (int64_t)hc[1], nB_run = (int64_t)hc[7];
-  float msC = 0, msB = 0, msL = 0, msT = 0;
+  // Per-launch windows from events recorded on each kernel's own stream right before and after it, with
+  // no host round trip inside any window (roofline denominators, bench.py):
+  //   classification ev0 -> ev1; engine L ev7 -> ev3 (stream2); engine B ev8 -> the later of its own end
+  //   (ev2) and the expansion launch's end (ev6, queued behind engine L on stream2); fallback ev9 -> ev10.
+  float msC = 0, msB = 0, msL = 0, msT = 0, msF = 0;
   cudaEventElapsedTime(&msC, h->ev[0], h->ev[1]);
-  cudaEventElapsedTime(&msB, h->ev[1], h->ev[2]);
-  if (gridB2 > 0) { float m2 = 0; cudaEventElapsedTime(&m2, h->ev[1], h->ev[6]); msB = std::max(msB, m2); }
-  if (nA > 0) cudaEventElapsedTime(&msL, h->ev[1], h->ev[3]);
-  cudaEventElapsedTime(&msT, h->ev[0], h->ev[4]);
+  if (nB > 0) {
+    cudaEventElapsedTime(&msB, h->ev[8], h->ev[2]);
+    if (gridB2 > 0) { float m2 = 0; cudaEventElapsedTime(&m2, h->ev[8], h->ev[6]); msB = std::max(msB, m2); }
+  }
+  if (nA > 0) cudaEventElapsedTime(&msL, h->ev[7], h->ev[3]);
+  if (ran_fallback) cudaEventElapsedTime(&msF, h->ev[9], h->ev[10]);
+  cudaEventElapsedTime(&msT, h->ev[0], ran_fallback ? h->ev[10] : h->ev[4]);
   if (h->k_prof && nA_run > 0) {
     unsigned long long pr[8];
     cudaMemcpy(pr, h->prof.p, 64, cudaMemcpyDeviceToHost);
@@ -686,14 +723,26 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   S.pd_tests = (int64_t)hc[2] + nA_run;  // bisected points count their classification test; + Lanczos points' one
   S.lanczos_iters = (int64_t)hc[5];
   {
-    const double n_int = (h->tz_j0 <= h->tz_j1) ? (double)(h->tz_j1 - h->tz_j0 + 1) : 0.0;
-    const double g_rows = (double)n - n_int + (n_int > 0 ? 1.0 : 0.0);  // rows that form G per round
-    const double rounds = (double)(int64_t)hc[2] / (double)kp.np + (double)nA_run + (double)nB_run;  // + classification
-    S.flops_bisect = (double)S.pd_tests * n * flops_ldl_row(kl, ku) + rounds * g_rows * flops_g_row(kl, ku);
+    // Executed FP64 flops, from the kernels' own row counters (a test stops early
+    // once every probe of the warp failed, so rows, not tests x n, measure the work). Per LDL^H row and
+    // probe: 4b^2 + 2b + 1. G rows:
+    //  - diagonal-constant (TZ) kernels form a point's boundary rows and its interior row once per point
+    //    from M's entries (4(b+1)(b+2) + 2 each) and read them in every test;
+    //  - general-band kernels form every row of every test from the A^H A expansion
+    //    (8(kl+1) + 8(ku+1) + 2, g_entry_aha), once per lane for the lane's NP probes.
+    const double nb1 = tzk ? (double)(h->tz_j0 + (n - 1 - h->tz_j1) + 1) : 0.0;
+    const double rc = (double)hc[16], r1 = (double)hc[17], r2 = (double)hc[19];
+    const double np1 = (double)kp.np, np2 = b2pair ? 1.0 : (double)kp.np;
+    const double ldl = flops_ldl_row(kl, ku);
+    const double pts_c = (double)(nA_run + nB_run), pts_b = (double)(int64_t)hc[3];
+    S.flops_classify = rc * ldl + (tzk ? pts_c * nb1 * flops_g_row(kl, ku) : rc * flops_g_row_aha(kl, ku));
+    S.flops_bisect = (r1 + r2) * ldl + (tzk ? pts_b * nb1 * flops_g_row(kl, ku)
+                                            : (r1 / np1 + r2 / np2) * flops_g_row_aha(kl, ku));
   }
   S.flops_lanczos = (double)hc[6] * n * flops_lu_row(kl, ku) + (double)hc[5] * n * flops_it_row(kl, ku);
   S.bytes_lanczos = (double)hc[6] * n * (16.0 * (s.NU + kl) + 4.0) + (double)hc[5] * n * bytes_it_row(kl, ku);
-  S.ms_bisect = msC + msB; S.ms_lanczos = msL; S.ms_total = msT;
+  S.ms_bisect = msB; S.ms_lanczos = msL; S.ms_total = msT; S.ms_classify = msC; S.ms_fallback = msF;
+  S.launches = 1 + (gridL > 0 ? 1 : 0) + (nB > 0 ? 1 : 0) + (gridB2 > 0 ? 1 : 0) + (ran_fallback ? 1 : 0);
   S.grid_bisect = (int32_t)(gridB + gridB2); S.grid_lanczos = (int32_t)gridL;
   if ((int64_t)(hc[3] + hc[6]) != P)
     return fail(h, PSB_ERR_CUDA, "internal: points finished " + std::to_string(hc[3] + hc[6]) + " != " +
@@ -820,6 +869,7 @@ int psb_smin_grid(psb_handle* h, const double* xs, int32_t nx, const double* ys,
     int rc = run_pipeline(h, h->zs.as<double2>(), d_idx, P, h->out.as<double>(), h->iters.as<int32_t>(),
                           h->status.as<int8_t>(), opts, st);
     if (rc != PSB_OK) return rc;
+    h->stats.launches += 1;  // k_grid_points
   } else {
     h->stats = psb_stats{};
   }

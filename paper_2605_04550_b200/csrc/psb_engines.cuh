@@ -42,6 +42,21 @@ struct BisArgs {
   int64_t tid_base;               // first thread index of this launch (engine B runs as one or two launches)
   double2* dyn_L;                 // DYN only: per-thread b*b ring
   double* dyn_D;                  // DYN only: per-thread 2b
+  unsigned long long* rowctr;     // nullable: += LDL^H rows x probes executed for points (roofline accounting)
+  const double2* __restrict__ RT; // general-band kernels: z-independent G-row coefficients, row-packed
+                                  //   (BisRow<KL,KU>::RW complex per row), staged per warp in shared memory
+};
+
+// Row-packed coefficient table of the general-band G rows (psb_set_matrix): row i holds
+//   [AHA_d = (A^H A)[i, i-d], d = 0..B | A[i, i-d], d = 0..KL | A[i-d, i], d = 1..KU]
+// so G[i, i-d] = AHA_d - conj(z) A[i, i-d] - z conj(A[i-d, i]) (g_entry_aha) reads one contiguous span.
+template <int KL, int KU>
+struct BisRow {
+  static constexpr int B = KL + KU;
+  static constexpr int RW = 2 * B + 2;  // complex per row
+  static constexpr int RB = 8;          // rows per stage (one unrolled block of the row loop)
+  static constexpr int SE = RB * RW;    // complex per stage
+  static constexpr int BYTES = 2 * SE * 16;  // two stages per warp
 };
 
 struct LanArgs {
@@ -462,6 +477,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
     const double2 zt = me ? z : czero();
     bool pd[NP];
     LogDet ld[NP];
+    int rows = a.n;  // LDL^H rows this warp executed in this round (tests stop early once every probe failed)
 #pragma unroll
     for (int q = 0; q < NP; q++) { pd[q] = true; ld[q].init(); }
     if constexpr (DYN) {
@@ -516,6 +532,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         J1 = min(max(a.tz_j1 - B, J0), a.n);
       }
       bool stop = false;
+      rows = 0;
       auto vote = [&]() {
         bool any = false;
 #pragma unroll
@@ -545,6 +562,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           loader(j + 1 + B);
           if (((j - j0) & 7) == 7) norm();
         }
+        rows += j - j0;
         norm();
       };
       // short edge segments: a plain row loop (keeps the unrolled code, and registers, to one body)
@@ -554,6 +572,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           gslot(B, j + 1 + B);
           if (((j - j0) & 7) == 7) norm();
         }
+        rows += j1 > j0 ? j1 - j0 : 0;
         norm();
       };
       if constexpr (TZ) {
@@ -561,9 +580,79 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         run8(J0, J1, [&](int) { pdw_load_row_g<KL, KU, NP>(Wn, B, gc, zz); });
         if (!stop) run1(J1, a.n);
       } else {
-        run8(0, a.n, [&](int i) { pdw_load_row<KL, KU, NP, true>(Wn, B, a.n, i, a.Ab, zt, zz, a.AHA); });
+        // General band: every lane of the warp walks the same rows in lockstep (the row loop and its
+        // early exit are warp-uniform), so the z-independent coefficients of the rows a block of 8
+        // steps consumes are one contiguous span of the table, copied into this warp's shared-memory
+        // stage by the whole warp (cp.async, 16 B per lane) one block ahead. The row loop then reads
+        // them as broadcast shared loads instead of issuing ~15 L2 loads per row one row ahead (the
+        // C5 kernel's long-scoreboard stall, profiles/r01_c5_ncu.md). Same values, same arithmetic:
+        // the bits do not change.
+        typedef BisRow<KL, KU> BR;
+        extern __shared__ __align__(16) double2 bis_stage[];
+        double2* stg = bis_stage + (threadIdx.x >> 5) * (2 * BR::SE);
+        auto fill = [&](int sidx, int i0) {
+          double2* dst = stg + sidx * BR::SE;
+#pragma unroll
+          for (int e0 = 0; e0 < BR::SE; e0 += 32) {
+            const int e = e0 + lane;
+            if (e0 + 32 <= BR::SE || e < BR::SE) {
+              const int i = i0 + e / BR::RW;
+              const int ic = i < a.n ? i : a.n - 1;
+              cp16z(dst + e, a.RT + (int64_t)ic * BR::RW + (e % BR::RW), i < a.n ? 16u : 0u);
+            }
+          }
+          cp_commit();
+        };
+        auto load_staged = [&](const double2* row, int i) {
+          double2 g[B + 1];
+#pragma unroll
+          for (int d = 0; d <= B; d++) {
+            g[d] = czero();
+            if (i < a.n && i - d >= 0) {
+              double2 v = row[d];
+              if (d <= KL) v = cfms_cj(v, zt, row[B + 1 + d]);                           // - conj(z) A[i, i-d]
+              if (d <= KU) v = cfms(v, zt, cconj(d == 0 ? row[B + 1] : row[B + 1 + KL + d]));  // - z conj(A[i-d, i])
+              g[d] = v;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < NP; q++) {
+#pragma unroll
+            for (int c = 0; c <= B; c++) Wn[q].W[B][c] = g[B - c];
+            Wn[q].W[B][B].x += (i < a.n) ? zz[q] : 1.0;
+            Wn[q].W[B][B].y = 0.0;
+          }
+        };
+        int j = 0, sidx = 0;
+        fill(0, 1 + B);
+        for (; !stop && j + 8 <= a.n; j += 8) {
+          fill(sidx ^ 1, j + 9 + B);  // the next block's rows (rows past n are zero-filled, never read)
+          cp_wait<1>();
+          __syncwarp();
+          const double2* st = stg + sidx * BR::SE;
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+            load_staged(st + u * BR::RW, j + u + 1 + B);
+          }
+          norm();
+          if ((j & 31) == 24) vote();
+          __syncwarp();  // every lane has read stage sidx before the next iteration refills it
+          sidx ^= 1;
+        }
+        cp_wait<0>();
+        __syncwarp();
+        for (; !stop && j < a.n; j++) {
+          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+          pdw_load_row<KL, KU, NP, true>(Wn, B, a.n, j + 1 + B, a.Ab, zt, zz, a.AHA);
+          if ((j & 7) == 7) norm();
+        }
+        rows = j;
+        norm();
       }
     }
+    // executed work for the roofline: LDL^H rows x probes of the lanes that hold a point
+    if (lane == 0 && a.rowctr) atomicAdd(a.rowctr, (unsigned long long)rows * (unsigned long long)(__popc(act) * NP));
     if (a.mode == 0) {
       // warp-aggregated appends keep a warp's consecutive (spatially adjacent) points together in
       // the lists, so engine-L warps get points with similar step counts (less lane divergence)

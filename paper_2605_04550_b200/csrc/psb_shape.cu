@@ -10,7 +10,7 @@ namespace {
 const KPair kSet = {-1, -1, &k_bisect<16, 16, true, 1, 1, false>, &k_bisect<16, 16, true, 1, 1, false>,
                     &k_bisect<16, 16, true, 1, 1, false>, &k_bisect<16, 16, true, 1, 1, false>,
                     &k_bisect<16, 16, true, 1, 1, false>, &k_bisect<16, 16, true, 1, 1, false>,
-                    &k_lanczos<16, 16, true, 2>, 0, 1, 1};
+                    &k_lanczos<16, 16, true, 2>, 0, 1, 1, 0};
 #else
 constexpr int D = RingDepth<PSB_KL, PSB_KU>::D;
 static_assert(PSB_NP * PSB_G == 2, "the pair variant (NP = 1, G = 2) must probe the same K = 2 shifts");
@@ -20,7 +20,7 @@ const KPair kSet = {PSB_KL, PSB_KU, &k_bisect<PSB_KL, PSB_KU, false, 1, 1, false
                     &k_bisect<PSB_KL, PSB_KU, false, PSB_NP, PSB_G, true>,
                     &k_bisect<PSB_KL, PSB_KU, false, 1, 2, false>,
                     &k_bisect<PSB_KL, PSB_KU, false, 1, 2, true>, &k_lanczos<PSB_KL, PSB_KU, false, D>,
-                    Ring<PSB_KL, PSB_KU, D>::BYTES, PSB_NP, PSB_G};
+                    Ring<PSB_KL, PSB_KU, D>::BYTES, PSB_NP, PSB_G, BisRow<PSB_KL, PSB_KU>::BYTES};
 #endif
 
 struct Registrar {

@@ -1,0 +1,47 @@
+"""A/B two library builds on full σ maps (development tool): bitwise equality and per-matrix kernel times.
+
+Usage: python tools/ab_maps.py C5 0,1,17,63 ablib/libpsb200_base.so paper_2605_04550_b200/libpsb200.so
+"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+name, mats, la, lb = sys.argv[1], [int(m) for m in sys.argv[2].split(",")], sys.argv[3], sys.argv[4]
+code = r"""
+import json, sys, numpy as np
+sys.path.insert(0, '.')
+from paper_2605_04550_b200 import configs, core
+c = configs.CONFIGS[sys.argv[1]]
+out = {}
+for m in [int(x) for x in sys.argv[2].split(',')]:
+    A = c.matrix(m)
+    core.full_pseudospectrum(A, c.grid)          # warm (upload, launch shapes)
+    best = None
+    for _ in range(2):
+        f = core.full_pseudospectrum(A, c.grid)
+        st = core.last_stats()
+        if best is None or st['ms_total'] < best['ms_total']:
+            best = st
+    np.save(f'/tmp/ab_{sys.argv[3]}_{m}.npy', f.values)
+    out[m] = {k: best[k] for k in ('ms_total', 'ms_bisect', 'ms_lanczos', 'ms_classify', 'n_bisect', 'n_lanczos')}
+print(json.dumps(out))
+"""
+res = {}
+for tag, lib in (("a", la), ("b", lb)):
+    r = subprocess.run([sys.executable, "-c", code, name, sys.argv[2], tag], capture_output=True, text=True,
+                       env={**os.environ, "PSB200_LIB": lib})
+    if r.returncode:
+        print(r.stderr[-3000:])
+        sys.exit(1)
+    res[tag] = json.loads(r.stdout.strip().splitlines()[-1])
+for m in mats:
+    a, b = np.load(f"/tmp/ab_a_{m}.npy"), np.load(f"/tmp/ab_b_{m}.npy")
+    eq = np.array_equal(a, b)
+    d = np.max(np.abs(a - b) / np.maximum(np.abs(a), 1e-300))
+    ta, tb = res["a"][str(m)], res["b"][str(m)]
+    print(f"{name} m={m}: bitwise {eq} (max rel {d:.2e}) | A total {ta['ms_total']:.1f} B {ta['ms_bisect']:.1f} "
+          f"L {ta['ms_lanczos']:.1f} C {ta.get('ms_classify', 0):.1f} | B total {tb['ms_total']:.1f} "
+          f"B {tb['ms_bisect']:.1f} L {tb['ms_lanczos']:.1f} C {tb.get('ms_classify', 0):.1f} ms")
