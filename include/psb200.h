@@ -16,6 +16,8 @@
  *   psb_predict_points    <- pseudospec/pipeline.py:169-172 _predict_points (+ features.py:129-164,
  *                            network.py:62-92,153-190)
  *   psb_region_select     <- pseudospec/pipeline.py:227-231 predicted_region (+ core.py:224-231 dilate)
+ *   psb_smin_selection    <- pseudospec/pipeline.py:292 restricted_field(A, grid, region) on that region
+ *                            (core.py:198-208), consuming the device-side compacted index list
  *   psb_recall_sweep      <- pseudospec/pipeline.py:258-259 the calibrate_threshold tau loop
  *   psb_write_field_csv   <- pseudospec/io.py:92-102 write_field_csv (host only, no handle)
  *   psb_write_mask_csv    <- pseudospec/io.py:105-115 write_mask_csv (host only, no handle)
@@ -122,9 +124,17 @@ int psb_predict_points(psb_handle* h, const double* params, const double* mean33
                        const double* zs, int64_t P, double* prob);
 
 /* predicted_region (pipeline.py:227-231): region = dilate(prob >= tau, k) on an (ny, nx) grid,
- * plus the row-major compacted index list of selected points (idx int64[ny*nx], *count). */
+ * plus the row-major compacted index list of selected points (idx int64[ny*nx] or NULL, *count). The
+ * compaction runs on the device and its list stays there as the handle's selection (psb_smin_selection). */
 int psb_region_select(psb_handle* h, const double* prob, int32_t ny, int32_t nx, double tau, int32_t k,
                       uint8_t* region, int64_t* idx, int64_t* count);
+
+/* restricted_field (core.py:198-208) on the selection the last psb_region_select left on the device (the
+ * row-major index list of its region, compacted by warp ballots and a block scan, np.flatnonzero order,
+ * core.py:204): no region upload and no host compaction. Same outputs and bits as psb_smin_grid with that
+ * region; PSB_ERR_PARAM when the handle holds no selection for an (ny, nx) grid. */
+int psb_smin_selection(psb_handle* h, const double* xs, int32_t nx, const double* ys, int32_t ny,
+                       const psb_opts* opts, double* sigma, int32_t* iters, int8_t* status, int64_t* fail_index);
 
 /* calibrate_threshold's inner loop (pipeline.py:258-259, _recall pipeline.py:234-238): for each
  * taus[t], recall[t] = |dilate(prob >= taus[t], k) & truth| / |truth| (1.0 when truth is empty).

@@ -281,6 +281,28 @@ def smin_at(A, z: complex, label: str = "matrix", *, device: int | None = None) 
     return float(smin_many(A, np.array([z], dtype=complex), label=label, device=device)[0])
 
 
+def _selection_call(A, grid: ComplexGrid, region, label, opts=None, device=None):
+    """restricted_field on the selection psb_region_select left on the device (`region` is that
+    selection's mask, used only to name a failing point)."""
+    xs = np.ascontiguousarray(grid.xs())
+    ys = np.ascontiguousarray(grid.ys())
+    band = as_band(A)
+    h = _lib.handle(device)
+    with h.lock:
+        _set_matrix(h, band)
+        out = np.empty(grid.shape)
+        fi = C.c_int64(-1)
+        rc = h.lib.psb_smin_selection(h.h, _lib._ptr(xs), grid.nx, _lib._ptr(ys), grid.ny,
+                                      C.byref(opts) if opts is not None else None, _lib._ptr(out), None, None,
+                                      C.byref(fi))
+        _last_stats.clear()
+        _last_stats.update(h.stats())
+        if rc != _lib.PSB_OK:
+            pts = grid.points().ravel()[np.flatnonzero(np.asarray(region).ravel())]
+            _raise(h, rc, label, pts, fi.value)
+    return out
+
+
 def _grid_call(A, grid: ComplexGrid, region, label, opts=None, device=None):
     xs = np.ascontiguousarray(grid.xs())
     ys = np.ascontiguousarray(grid.ys())

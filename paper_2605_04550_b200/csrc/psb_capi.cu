@@ -94,7 +94,11 @@ struct psb_handle {
   DevBuf xs, ys, prof;
   PinBuf pin;
   // predictor
-  DevBuf params, feat, eig, prob, region, idx;
+  DevBuf params, feat, eig, prob, region, idx, selblk;
+  // current device selection (psb_region_select / the region path): h->outidx[0, sel_P) of an sel_N grid
+  bool sel_valid = false;
+  int64_t sel_N = 0, sel_P = 0;
+  int32_t sel_nx = 0;
   psb_stats stats{};
 };
 
@@ -200,7 +204,7 @@ void psb_destroy(psb_handle* h) {
   DeviceGuard dg(h->device);
   DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->RT, &h->v1, &h->offmin, &h->gbuf, &h->listF, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
                     &h->counters, &h->scratch, &h->pivs, &h->dynL, &h->dynD, &h->xs, &h->ys, &h->params,
-                    &h->feat, &h->eig, &h->prob, &h->region, &h->idx};
+                    &h->feat, &h->eig, &h->prob, &h->region, &h->idx, &h->selblk};
   for (DevBuf* b : bufs) b->release();
   h->pin.release();
   for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
@@ -816,51 +820,77 @@ int psb_smin_points(psb_handle* h, const double* zs, int64_t P, const psb_opts* 
   return check_status(h, stat_h, nullptr, P, fail_index);
 }
 
-int psb_smin_grid(psb_handle* h, const double* xs, int32_t nx, const double* ys, int32_t ny, const uint8_t* region,
-                  const psb_opts* opts, double* sigma, int32_t* iters, int8_t* status, int64_t* fail_index) {
-  if (!h) return PSB_ERR_PARAM;
-  std::lock_guard<std::mutex> lk(h->mu);
+}  // extern "C"
+
+// Ordered compaction of a device mask into h->outidx (np.flatnonzero order, core.py:204): three kernels
+// and one 8-byte read-back of the count (the pipeline sizes its launches on the host).
+static int select_device(psb_handle* h, const uint8_t* d_mask, int64_t N, cudaStream_t st, int64_t* P) {
+  const int64_t nblk = (N + SEL_TPB - 1) / SEL_TPB;
+  CK(h->outidx.ensure(sizeof(int64_t) * std::max<int64_t>(N, 1)));
+  CK(h->selblk.ensure(sizeof(unsigned long long) * (nblk + 1)));
+  unsigned long long* blk = h->selblk.as<unsigned long long>();
+  int64_t* d_count = reinterpret_cast<int64_t*>(blk + nblk);
+  k_sel_count<<<(unsigned)nblk, SEL_TPB, 0, st>>>(d_mask, N, blk);
+  k_sel_scan<<<1, SEL_TPB, 0, st>>>(blk, nblk, d_count);
+  k_sel_scatter<<<(unsigned)nblk, SEL_TPB, 0, st>>>(d_mask, N, blk, h->outidx.as<int64_t>());
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(h->pin.at<char>(0), d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *P = *h->pin.at<int64_t>(0);
+  h->sel_N = N;
+  h->sel_P = *P;
+  return PSB_OK;
+}
+
+// Shared body of psb_smin_grid (mode 0: full grid, mode 1: host region uploaded and compacted on the
+// device) and psb_smin_selection (mode 2: the handle's current selection from psb_region_select).
+static int grid_eval(psb_handle* h, const double* xs, int32_t nx, const double* ys, int32_t ny, int mode,
+                     const uint8_t* region, const psb_opts* opts, double* sigma, int32_t* iters, int8_t* status,
+                     int64_t* fail_index) {
   if (fail_index) *fail_index = -1;
   if (!h->have_matrix) return fail(h, PSB_ERR_PARAM, "no matrix set");
   if (!xs || !ys || !sigma || nx < 1 || ny < 1) return fail(h, PSB_ERR_PARAM, "bad grid arguments");
   const int64_t N = (int64_t)nx * ny;
+  if (mode == 2 && (!h->sel_valid || h->sel_N != N || h->sel_nx != nx))
+    return fail(h, PSB_ERR_PARAM, "no device selection for this grid (call psb_region_select first)");
   DeviceGuard dg(h->device);
   cudaStream_t st = h->stream;
-  // pinned staging: [xs | ys | idx (restricted) | sigma | iters | status]
-  const size_t ox = 0, oy = ox + 8 * (size_t)nx, oidx = oy + 8 * (size_t)ny;
-  const size_t os = oidx + (region ? 8 * (size_t)N : 0), oi = os + 8 * (size_t)N, ot = oi + 4 * (size_t)N;
+  // pinned staging: [count | xs | ys | sigma | iters | status]
+  const size_t ox = 64, oy = ox + 8 * (size_t)nx, os = oy + 8 * (size_t)ny, oi = os + 8 * (size_t)N,
+               ot = oi + 4 * (size_t)N;
   CK(h->pin.ensure(ot + (size_t)N));
   std::memcpy(h->pin.at<char>(ox), xs, 8 * (size_t)nx);
   std::memcpy(h->pin.at<char>(oy), ys, 8 * (size_t)ny);
-  // row-major compaction of the region (core.py:204 np.flatnonzero order)
-  int64_t P = N;
-  int64_t* idx = nullptr;
-  if (region) {
-    idx = h->pin.at<int64_t>(oidx);
-    P = 0;
-    for (int64_t g = 0; g < N; g++)
-      if (region[g]) idx[P++] = g;
-  }
   CK(h->out.ensure(sizeof(double) * N));
   CK(h->iters.ensure(sizeof(int32_t) * N));
   CK(h->status.ensure(sizeof(int8_t) * N));
-  CK(h->zs.ensure(sizeof(double2) * std::max<int64_t>(P, 1)));
   CK(h->xs.ensure(8 * (size_t)nx));
   CK(h->ys.ensure(8 * (size_t)ny));
   CK(cudaMemcpyAsync(h->xs.p, h->pin.at<char>(ox), 8 * (size_t)nx, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(h->ys.p, h->pin.at<char>(oy), 8 * (size_t)ny, cudaMemcpyHostToDevice, st));
+  int64_t P = N;
   const int64_t* d_idx = nullptr;
-  if (region) {
+  int extra = 0;  // kernels launched here besides the pipeline
+  if (mode == 1) {
+    h->sel_valid = false;  // the region path reuses the selection buffers
+    CK(h->region.ensure(N));
+    CK(cudaMemcpyAsync(h->region.p, region, N, cudaMemcpyHostToDevice, st));
+    int rc = select_device(h, h->region.as<uint8_t>(), N, st, &P);
+    if (rc != PSB_OK) return rc;
+    extra += 3;
+  } else if (mode == 2) {
+    P = h->sel_P;
+  }
+  if (mode != 0) {
+    d_idx = h->outidx.as<int64_t>();
     // NaN marks unevaluated points (core.py:203); the full grid overwrites every entry
-    CK(cudaMemsetAsync(h->out.p, 0xff, sizeof(double) * N, st));  // 0xff.. is a NaN pattern
+    k_fill_nan<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(h->out.as<double>(), N);
+    CK(cudaGetLastError());
     CK(cudaMemsetAsync(h->iters.p, 0, sizeof(int32_t) * N, st));
     CK(cudaMemsetAsync(h->status.p, 0, sizeof(int8_t) * N, st));
-    if (P > 0) {
-      CK(h->outidx.ensure(sizeof(int64_t) * P));
-      CK(cudaMemcpyAsync(h->outidx.p, idx, sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
-      d_idx = h->outidx.as<int64_t>();
-    }
+    extra += 1;
   }
+  CK(h->zs.ensure(sizeof(double2) * std::max<int64_t>(P, 1)));
   if (P > 0) {
     // shifts from the grid axes on the device: z = xs[g % nx] + i ys[g / nx] (the host's linspace bits)
     k_grid_points<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(h->xs.as<double>(), nx, h->ys.as<double>(), d_idx, P,
@@ -869,10 +899,11 @@ int psb_smin_grid(psb_handle* h, const double* xs, int32_t nx, const double* ys,
     int rc = run_pipeline(h, h->zs.as<double2>(), d_idx, P, h->out.as<double>(), h->iters.as<int32_t>(),
                           h->status.as<int8_t>(), opts, st);
     if (rc != PSB_OK) return rc;
-    h->stats.launches += 1;  // k_grid_points
+    extra += 1;  // k_grid_points
   } else {
     h->stats = psb_stats{};
   }
+  h->stats.launches += extra;
   CK(cudaMemcpyAsync(h->pin.at<char>(os), h->out.p, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
   if (iters) CK(cudaMemcpyAsync(h->pin.at<char>(oi), h->iters.p, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h->pin.at<char>(ot), h->status.p, sizeof(int8_t) * N, cudaMemcpyDeviceToHost, st));
@@ -880,11 +911,32 @@ int psb_smin_grid(psb_handle* h, const double* xs, int32_t nx, const double* ys,
   std::memcpy(sigma, h->pin.at<char>(os), 8 * (size_t)N);
   if (iters) std::memcpy(iters, h->pin.at<char>(oi), 4 * (size_t)N);
   if (status) std::memcpy(status, h->pin.at<char>(ot), (size_t)N);
-  // canonical quiet NaN off-region (the memset pattern is a NaN; normalise for bitwise tests)
-  if (region)
-    for (int64_t g = 0; g < N; g++)
-      if (!region[g]) sigma[g] = std::numeric_limits<double>::quiet_NaN();
-  return check_status(h, h->pin.at<int8_t>(ot), idx, P, fail_index);
+  const int8_t* stat_h = h->pin.at<int8_t>(ot);
+  if (mode == 0) return check_status(h, stat_h, nullptr, P, fail_index);
+  // restricted: off-region status is 0, so any failure is a selected point; only then is the point's rank
+  // in the selection (the index NumericalError names, core.py:163-165) looked up, from the device list
+  bool bad = false;
+  for (int64_t g = 0; g < N && !bad; g++) bad = stat_h[g] >= 3;
+  if (!bad) return PSB_OK;
+  std::vector<int64_t> idx((size_t)P);
+  CK(cudaMemcpy(idx.data(), d_idx, sizeof(int64_t) * P, cudaMemcpyDeviceToHost));
+  return check_status(h, stat_h, idx.data(), P, fail_index);
+}
+
+extern "C" {
+
+int psb_smin_grid(psb_handle* h, const double* xs, int32_t nx, const double* ys, int32_t ny, const uint8_t* region,
+                  const psb_opts* opts, double* sigma, int32_t* iters, int8_t* status, int64_t* fail_index) {
+  if (!h) return PSB_ERR_PARAM;
+  std::lock_guard<std::mutex> lk(h->mu);
+  return grid_eval(h, xs, nx, ys, ny, region ? 1 : 0, region, opts, sigma, iters, status, fail_index);
+}
+
+int psb_smin_selection(psb_handle* h, const double* xs, int32_t nx, const double* ys, int32_t ny,
+                       const psb_opts* opts, double* sigma, int32_t* iters, int8_t* status, int64_t* fail_index) {
+  if (!h) return PSB_ERR_PARAM;
+  std::lock_guard<std::mutex> lk(h->mu);
+  return grid_eval(h, xs, nx, ys, ny, 2, nullptr, opts, sigma, iters, status, fail_index);
 }
 
 }  // extern "C"
@@ -983,17 +1035,23 @@ int psb_region_select(psb_handle* h, const double* prob, int32_t ny, int32_t nx,
   const int64_t N = (int64_t)ny * nx;
   DeviceGuard dg(h->device);
   cudaStream_t st = h->stream;
+  h->sel_valid = false;
   CK(h->prob.ensure(sizeof(double) * N));
   CK(h->region.ensure(N));
+  CK(h->pin.ensure(64));
   CK(cudaMemcpyAsync(h->prob.p, prob, sizeof(double) * N, cudaMemcpyHostToDevice, st));
   k_region<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(h->prob.as<double>(), ny, nx, tau, k, h->region.as<uint8_t>());
   CK(cudaGetLastError());
+  // the selected points' row-major index list stays on the device for psb_smin_selection
+  int64_t P = 0;
+  int rc = select_device(h, h->region.as<uint8_t>(), N, st, &P);
+  if (rc != PSB_OK) return rc;
   CK(cudaMemcpyAsync(region, h->region.p, N, cudaMemcpyDeviceToHost, st));
+  if (idx && P > 0) CK(cudaMemcpyAsync(idx, h->outidx.p, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  int64_t c = 0;
-  for (int64_t g = 0; g < N; g++)
-    if (region[g]) { if (idx) idx[c] = g; c++; }
-  if (count) *count = c;
+  if (count) *count = P;
+  h->sel_valid = true;
+  h->sel_nx = nx;
   return PSB_OK;
 }
 

@@ -150,6 +150,82 @@ __global__ void k_region(const double* __restrict__ prob, int ny, int nx, double
   region[g] = v;
 }
 
+// ---------------------------------------------------------------- ordered stream compaction
+// idx = np.flatnonzero(mask) (core.py:204, the order restricted_field evaluates and places points in)
+// on the device: (1) per-block counts from warp ballots, (2) one block scans the block counts,
+// (3) every block re-ballots its elements and writes each selected grid index at block offset +
+// warp offset + lane rank. Blocks of SEL_TPB elements, one element per thread.
+constexpr int SEL_TPB = 1024;
+
+__device__ __forceinline__ unsigned sel_block_scan(unsigned bal, unsigned* wsum) {
+  // returns this warp's exclusive offset within the block; wsum[32] scratch (shared)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned v = (lane < (int)(blockDim.x >> 5)) ? wsum[lane] : 0u;
+    unsigned inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    wsum[lane] = inc - v;  // exclusive
+  }
+  __syncthreads();
+  return wsum[warp];
+}
+
+__global__ void __launch_bounds__(SEL_TPB) k_sel_count(const uint8_t* __restrict__ mask, int64_t N,
+                                                        unsigned long long* __restrict__ blk) {
+  __shared__ unsigned wsum[32];
+  const int64_t g = (int64_t)blockIdx.x * SEL_TPB + threadIdx.x;
+  const unsigned bal = __ballot_sync(0xffffffffu, g < N && mask[g] != 0);
+  const unsigned off = sel_block_scan(bal, wsum);
+  if (threadIdx.x == blockDim.x - 1) blk[blockIdx.x] = off + __popc(bal);
+}
+
+// exclusive scan of nblk block counts in place (one block of SEL_TPB threads, chunked); total -> *count
+__global__ void __launch_bounds__(SEL_TPB) k_sel_scan(unsigned long long* __restrict__ blk, int64_t nblk,
+                                                       int64_t* __restrict__ count) {
+  __shared__ unsigned long long part[SEL_TPB];
+  unsigned long long carry = 0;
+  for (int64_t c0 = 0; c0 < nblk; c0 += SEL_TPB) {
+    const int64_t i = c0 + threadIdx.x;
+    const unsigned long long v = i < nblk ? blk[i] : 0ull;
+    part[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < SEL_TPB; o <<= 1) {  // Hillis-Steele inclusive scan
+      const unsigned long long y = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0ull;
+      __syncthreads();
+      part[threadIdx.x] += y;
+      __syncthreads();
+    }
+    if (i < nblk) blk[i] = carry + part[threadIdx.x] - v;
+    carry += part[SEL_TPB - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = (int64_t)carry;
+}
+
+__global__ void __launch_bounds__(SEL_TPB) k_sel_scatter(const uint8_t* __restrict__ mask, int64_t N,
+                                                          const unsigned long long* __restrict__ blk,
+                                                          int64_t* __restrict__ idx) {
+  __shared__ unsigned wsum[32];
+  const int64_t g = (int64_t)blockIdx.x * SEL_TPB + threadIdx.x;
+  const bool on = g < N && mask[g] != 0;
+  const unsigned bal = __ballot_sync(0xffffffffu, on);
+  const unsigned off = sel_block_scan(bal, wsum);
+  const int lane = threadIdx.x & 31;
+  if (on) idx[blk[blockIdx.x] + off + __popc(bal & ((1u << lane) - 1u))] = g;
+}
+
+// canonical quiet NaN everywhere (restricted_field's unevaluated points, core.py:203)
+__global__ void k_fill_nan(double* __restrict__ out, int64_t N) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < N) out[g] = __longlong_as_double(0x7ff8000000000000ll);
+}
+
 // calibrate_threshold's tau loop (pipeline.py:258-259) in one pass: dilate(prob >= tau, k) at a
 // pixel is (max of prob over the clipped k x k window) >= tau, so every tau is decided from one
 // window maximum. counts[t] += #{truth pixels with wmax >= taus[t]} (warp ballots, then one

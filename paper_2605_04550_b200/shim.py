@@ -4,7 +4,9 @@ The reference has no plugin registry or FFI: its σ callers look `smin_many`,
 `full_pseudospectrum` and `restricted_field` up as module globals (core.py:187,207;
 pipeline.py:17-18; cli.py:22), and the predictor through `pipeline._predict_points`
 (pipeline.py:179,200,222); the field/mask writers as `io.write_*_csv` (cli.py:149-151).
-`install()` rebinds exactly those names (the substitution-point
+`install()` rebinds exactly those names, plus `pipeline.global_features` (the bitwise restatement,
+cached per matrix) and the corpus-level `benchmark` / `build_dataset`, which prefetch every matrix's
+host features on host threads so they overlap the GPU work (the substitution-point
 precedent is the reference's own tests, tests/test_pipeline.py:188 monkeypatching
 `pipeline.predict_map`), so every caller — cmd_compute, build_dataset, calibrate_threshold,
 hybrid_pseudospectrum, benchmark — runs on the GPU unchanged. Results come back as the
@@ -119,6 +121,7 @@ def install(ps=None, predictor: bool = True):
                 raise rcore.ParameterError("validation corpus is empty")
             taus = rpipe.CAL_TAUS
             recalls = np.empty((len(val_corpus), taus.size))
+            pipeline.prefetch_global_features([(_real(e.matrix), e.probe_seed) for e in val_corpus])
             for row, entry in enumerate(val_corpus):
                 fld = rpipe.full_pseudospectrum(entry.matrix, grid, label=f"matrix {entry.index}",
                                                 workers=workers)
@@ -134,10 +137,48 @@ def install(ps=None, predictor: bool = True):
                                                recalls=recalls)
             return rpipe.CalibrationReport(taus.copy(), med, p10, tau_star=None, passed=False, recalls=recalls)
 
+        rfeat = importlib.import_module(ps.__name__ + ".features")
+
+        @tr
+        def global_features(A, probe_seed=0):
+            # the reference's f1..f30 (features.py:63-117) restated bit for bit, BLAS pinned to one thread,
+            # cached per (matrix, seed) and prefetched on host threads by the corpus-level calls below
+            gf = pipeline.global_features(_real(A), probe_seed=probe_seed)
+            return rfeat.GlobalFeatures(values=gf.values.copy(), eigvals=gf.eigvals.copy(),
+                                        singvals=gf.singvals.copy())
+
+        def _prefetch(corpus):
+            pipeline.prefetch_global_features([(_real(e.matrix), e.probe_seed) for e in corpus])
+
+        orig_benchmark, orig_build = rpipe.benchmark, rpipe.build_dataset
+
+        @functools.wraps(orig_benchmark)
+        def benchmark(bundle, test_corpus, grid, eps, seed=0, baseline=False, workers=1):
+            # every matrix's host features start on host threads now and overlap the GPU sweeps; the
+            # σ work itself is on the GPU, so the reference's process pool is not used (workers=1)
+            _prefetch(test_corpus)
+            return orig_benchmark(bundle, test_corpus, grid, eps, seed=seed, baseline=baseline, workers=1)
+
+        @functools.wraps(orig_build)
+        def build_dataset(corpus, grid, eps, seed, workers=1):
+            if not corpus:
+                raise rcore.ParameterError("corpus is empty")
+            _prefetch(corpus)
+            # workers=1: forked pool children must not inherit the CUDA context
+            return orig_build(corpus, grid, eps, seed, workers=1)
+
         _patch(rpipe, "_predict_points", _predict_points)
         _patch(rpipe, "predicted_region", predicted_region)
         _patch(rpipe, "calibrate_threshold", calibrate_threshold)
         _patch(rcli, "calibrate_threshold", calibrate_threshold)
+        _patch(rpipe, "global_features", global_features)
+        _patch(rpipe, "benchmark", benchmark)
+        _patch(rpipe, "build_dataset", build_dataset)
+        for name, fn in (("benchmark", benchmark), ("build_dataset", build_dataset)):
+            if hasattr(ps, name):
+                _patch(ps, name, fn)
+            if hasattr(rcli, name):
+                _patch(rcli, name, fn)
     return ps
 
 

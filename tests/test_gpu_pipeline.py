@@ -71,6 +71,46 @@ def test_region_kernel_matches_host_dilation(gpu):
         assert np.array_equal(pipeline.predicted_region(prob, tau), core.dilate(prob >= tau, 5))
 
 
+@pytest.mark.parametrize("shape,frac", [((37, 53), 0.3), ((1, 1), 1.0), ((8, 128), 0.0), ((1024, 1025), 0.23),
+                                        ((3, 1500), 1.0), ((700, 1700), 0.001)])
+def test_device_compaction_is_flatnonzero(gpu, shape, frac):
+    """psb_region_select's device compaction (ballots + block scan; >1024 blocks exercises the chunked scan)
+    gives np.flatnonzero's list (core.py:204), and its region dilate(prob >= tau, 5)."""
+    import ctypes as C
+    from paper_2605_04550_b200 import _lib
+    rng = np.random.default_rng(shape[0] + shape[1])
+    prob = np.where(rng.random(shape) < frac, 0.9, 0.1)
+    ny, nx = shape
+    region = np.empty(shape, dtype=np.uint8)
+    idx = np.full(ny * nx, -7, dtype=np.int64)
+    cnt = C.c_int64(-1)
+    h = _lib.handle()
+    with h.lock:
+        rc = h.lib.psb_region_select(h.h, _lib._ptr(np.ascontiguousarray(prob)), ny, nx, 0.5, 5, _lib._ptr(region),
+                                     _lib._ptr(idx), C.byref(cnt))
+    assert rc == 0
+    want = core.dilate(prob >= 0.5, 5)
+    assert np.array_equal(region.astype(bool), want)
+    flat = np.flatnonzero(want.ravel())
+    assert cnt.value == flat.size
+    assert np.array_equal(idx[: flat.size], flat)
+
+
+def test_selection_equals_restricted_field_bitwise(gpu, bundle):
+    """hybrid_pseudospectrum's device-side selection path == restricted_field(region) == the full field."""
+    c = configs.CONFIGS["C1"]
+    A = c.matrix()
+    prob, _ = pipeline.hierarchical_predict(bundle, A.todense().real, c.grid)
+    region = pipeline.predicted_region(prob, bundle.tau_star)
+    got = core._selection_call(A, c.grid, region, "m")
+    want = core.restricted_field(A, c.grid, region)
+    assert np.array_equal(got, want.values, equal_nan=True)
+    assert np.all(np.isnan(got[~region])) and not np.any(np.isnan(got[region]))
+    # a stale selection for another grid shape is refused (ParameterError), not silently used
+    with pytest.raises(core.ParameterError):
+        core._selection_call(A, core.make_grid(-1, 3, -3.5, 3.5, 20, 20), np.ones((20, 20), bool), "m")
+
+
 def _recall_loop(prob, truth, taus, k):
     """The reference's tau loop, restated (pipeline.py:234-238,258-259; dilate = core.py:224-231)."""
     from scipy.ndimage import binary_dilation
