@@ -264,16 +264,30 @@ def cpu_baseline_line(cfg, name) -> dict:
 
 
 # ----------------------------------------------------------------------------- our arm
-def run_guided(cfg, grid, args) -> dict:
-    """BASELINE C2's MLP-guided run (pipeline.py:273-297): hierarchical prediction (K2) with the bundle
-    the reference trained and calibrated (tests/golden/model_grcar.npz), 5x5-dilated region, restricted
-    σ sweep (K1). Reports the reference's own timing split and its metrics against the full map."""
+def run_guided(name, cfg, args) -> dict:
+    """The MLP-guided run (pipeline.py:273-297): hierarchical prediction (K2), 5x5-dilated region, restricted
+    σ sweep on the device-side selection (K1). C1/C2 (BASELINE configs[1]) use the bundle the reference
+    trained and calibrated on a Grcar family (tests/golden/model_grcar.npz, eps 0.01); C4 (configs[3])
+    the one it trained on a convection-diffusion family (model_c4.npz), in the exact power-of-two units
+    oracle/make_guided_c4.py explains. Reports the reference's timing split and its metrics against the
+    full map (pipeline.py:300-331)."""
     import torch
 
     from paper_2605_04550_b200 import core, pipeline
-    bundle = pipeline.load_npz(ROOT / "tests" / "golden" / "model_grcar.npz")
-    A = cfg.matrix(0).todense().real
-    eps = 0.01
+    grid = cfg.grid
+    if name == "C4":
+        mz = np.load(ROOT / "tests" / "golden" / "model_c4.npz")
+        bundle = pipeline.load_npz(ROOT / "tests" / "golden" / "model_c4.npz")
+        S, eps = float(mz["scale"]), float(mz["eps"])
+        A0 = cfg.matrix(0)
+        Ab = core.BandMatrix(A0.band * S, A0.kl, A0.ku)
+        grid = core.make_grid(grid.x_min * S, grid.x_max * S, grid.y_min * S, grid.y_max * S, grid.nx, grid.ny)
+        A = Ab.todense().real.copy()
+        units = f"A and z scaled by {S:g} (exact power of two)"
+    else:
+        bundle = pipeline.load_npz(ROOT / "tests" / "golden" / "model_grcar.npz")
+        A = cfg.matrix(0).todense().real
+        Ab, eps, units = cfg.matrix(0), 0.01, "as configured"
     res = None
     t_nn, t_r = [], []
     pipeline.clear_feature_cache()
@@ -286,7 +300,7 @@ def run_guided(cfg, grid, args) -> dict:
         if it >= args.warmup:
             t_nn.append(res.t_nn)
             t_r.append(res.t_restricted)
-    full = core.full_pseudospectrum(cfg.matrix(0), grid)
+    full = core.full_pseudospectrum(Ab, grid)
     truth = full.values <= eps
     region = res.region
     tp = int((region & truth).sum())
@@ -295,8 +309,9 @@ def run_guided(cfg, grid, args) -> dict:
     coverage = float(tp / truth.sum()) if truth.sum() else 1.0
     same = bool(np.array_equal(res.field.values[region], full.values[region]))
     tn, tr = float(np.median(t_nn)), float(np.median(t_r))
-    return {"eps": eps, "tau_star": bundle.tau_star, "nn_evaluations": int(res.nn_evaluations),
-            "grid_fraction": float(region.mean()), "t_nn_s": tn, "t_nn_cold_s": t_cold, "t_restricted_s": tr, "t_hybrid_s": tn + tr,
+    return {"eps": eps, "units": units, "tau_star": bundle.tau_star, "nn_evaluations": int(res.nn_evaluations),
+            "grid_fraction": float(region.mean()), "t_nn_s": tn, "t_nn_cold_s": t_cold,
+            "t_restricted_s": tr, "t_hybrid_s": tn + tr,
             "grid_points_per_s": grid.size / (tn + tr), "recall": recall, "coverage": coverage,
             "restricted_equals_full_bitwise": same,
             "note": "t_nn: median over timed calls, host global_features served from the per-matrix cache; "
@@ -510,8 +525,8 @@ def run_ours(args, rank, world, local_rank):
     model = lu_solve_model(n_, kl_, ku_, S, fp64_peak, hbm_peak)
 
     guided = None
-    if rank == 0 and world == 1 and name in ("C1", "C2") and not args.no_guided:
-        guided = run_guided(cfg, grid, args)
+    if rank == 0 and world == 1 and name in ("C1", "C2", "C4") and not args.no_guided:
+        guided = run_guided(name, cfg, args)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_line(cfg, name)

@@ -130,11 +130,12 @@ PSB_HD Shape make_shape(int n, int kl, int ku) {
 // as zgbtrf). Returns false on an exactly zero pivot (M singular in floating point).
 struct NoRowHook {
   template <int N>
-  PSB_HD void operator()(int, const double2 (&)[N]) const {}
+  PSB_HD bool operator()(int, const double2 (&)[N]) const { return true; }
 };
 
 // `hook(j, u)` sees each finished U row (u[0..W-1] = U', u[W] = rinv) in forward order, so a
-// forward sweep that needs exactly these rows can run fused with the factorization.
+// forward sweep that needs exactly these rows can run fused with the factorization. A hook that
+// returns false ends the factorization there (lu_factor returns false, as for an exact zero pivot).
 template <int KLM, int KUM, bool DYN, class RowHook = NoRowHook>
 PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z, LV FU, LV FL, LVb piv,
                       RowHook hook = RowHook()) {
@@ -201,7 +202,7 @@ PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z,
       }
     u[DYN ? WM : W] = ri;  // static shapes: u[W] = rinv (the hook is static-shape only)
     FU.put(rb + W, ri);
-    hook(j, u);
+    if (!hook(j, u)) return false;
 #pragma unroll
     for (int r = 1; r <= KLM; r++) {
       if (r <= kl) {

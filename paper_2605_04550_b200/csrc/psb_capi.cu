@@ -81,7 +81,7 @@ struct psb_handle {
   long long k_lwarps = 0;
   int k_btpb = 128;
   double k_tau = 0.0;
-  bool k_bexpand = true, k_fallback = true;
+  bool k_bexpand = true, k_fallback = true, k_seq = false;
   int k_bvariant = 0;
   struct FitEntry { const void* f; int lkey, btpb, tpb, occ, occFull; int64_t threads; int wregs; };
   std::vector<FitEntry> fit_cache;  // engine-B launch shapes per (kernel, engine-L share)
@@ -189,6 +189,7 @@ int psb_create(int device, psb_handle** out) {
   h->k_bexpand = getenv("PSB_NOBEXP") == nullptr;
   h->k_fallback = getenv("PSB_NOFALLBACK") == nullptr;
   h->k_bvariant = getenv("PSB_BVARIANT") ? atoi(getenv("PSB_BVARIANT")) : 0;
+  h->k_seq = getenv("PSB_SEQ") != nullptr;  // dev: engine B after engine L (full occupancy) instead of beside it
   h->k_tau = getenv("PSB_TAU") ? atof(getenv("PSB_TAU")) : 0.0;  // dev: default engine split
   h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 0;  // 0: pick per launch
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
@@ -462,6 +463,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.tz_j1 = h->k_toeplitz ? h->tz_j1 : 0;
   const int64_t gridC = std::max<int64_t>(1, std::min<int64_t>((int64_t)occB * h->num_sms, (P + 127) / 128));
   int64_t gridB = (int64_t)occB * h->num_sms, gridB2 = 0;
+  cudaStream_t sB = st;  // engine B's stream (stream2 behind engine L in the sequential mode)
   bool b2pair = false;  // the expansion launch runs the pair variant (one probe per lane)
   if (dyn) {
     const int b = std::max(kl + ku, 1);
@@ -609,6 +611,8 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     const int tpbB = fc.tpb, occShare = fc.occ, occFull = fc.occFull;
     const int64_t wantB = (nB * kp.g + tpbB - 1) / tpbB;
     gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, wantB));
+    const bool seq = h->k_seq && nA > 0 && gridL > 0;
+    if (seq) gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occFull * h->num_sms, wantB));
     // A second launch, queued behind engine L on its stream, takes the SM share engine L releases when
     // it finishes (both launches pull from the same work counter), so a long bisection tail runs at
     // full occupancy instead of the share it had next to engine L.
@@ -616,7 +620,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     // late starters' last points stretch the tail by a point's latency (C3: +4%; C5: -15%).
     bis_fn fB2 = kp.bm;
     int tpb2 = tpbB, g2 = kp.g;
-    if (nA > 0 && gridL > 0 && h->k_bexpand) {
+    if (nA > 0 && gridL > 0 && h->k_bexpand && !seq) {
       const int64_t extra = std::max<int64_t>(0, std::min<int64_t>((int64_t)occFull * h->num_sms, wantB) - gridB);
       if (nB * kp.g >= 4 * (gridB + extra) * tpbB) {
         gridB2 = extra;  // long list: the same (wide) variant at full occupancy (C5 1157 -> 975 ms)
@@ -645,8 +649,9 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
       CK(h->dynD.ensure(sizeof(double) * (size_t)ba.gb_T * 2 * std::max(kl + ku, 1)));
       ba.dyn_L = h->dynL.as<double2>(); ba.dyn_D = h->dynD.as<double>();
     }
-    CK(cudaEventRecord(h->ev[8], st));
-    kp.bm<<<(unsigned)gridB, tpbB, bsm(tpbB), st>>>(ba);
+    sB = seq ? h->stream2 : st;
+    CK(cudaEventRecord(h->ev[8], sB));
+    kp.bm<<<(unsigned)gridB, tpbB, bsm(tpbB), sB>>>(ba);
     CK(cudaGetLastError());
     if (gridB2 > 0) {
       BisArgs b2 = ba;
@@ -659,7 +664,8 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   } else {
     gridB = 0;
   }
-  CK(cudaEventRecord(h->ev[2], st));
+  CK(cudaEventRecord(h->ev[2], sB));
+  if (sB != st) CK(cudaStreamWaitEvent(st, h->ev[2], 0));
   if (nA > 0) CK(cudaStreamWaitEvent(st, h->ev[3], 0));
   if (gridB2 > 0) CK(cudaStreamWaitEvent(st, h->ev[6], 0));
   CK(cudaEventRecord(h->ev[4], st));

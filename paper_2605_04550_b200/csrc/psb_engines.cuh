@@ -838,15 +838,22 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
         for (int d = 0; d <= W; d++) acc[d] = czero();
         const double2* __restrict__ v1b = a.v1b;
         double2 vnext = v1b[0];  // one row ahead
+        // A non-finite t_j = (U^{-H} v1)_j decides the point already: S2 would carry it into
+        // nu = ||M^{-H} v1|| (every T entry reaches nu's sum), and a non-finite nu finishes the point as
+        // singular to working precision (sigma = 0, status 2) - the outcome of an exact zero pivot. So
+        // the factorization stops at that row (the same results; deep inside the pseudospectrum of a
+        // strongly non-normal band, U^{-H} v1 overflows a few hundred rows in, C5).
         ok = lu_factor<KL, KU, DYN>(s, a.Ab, z, FU, FL, piv, [&](int j, const double2 (&u)[W + 1]) {
           const double2 r = vnext;
           if (j + 1 < n) vnext = v1b[j + 1];
           Rn.put(j, r);
           const double2 tp = cadd(r, acc[0]);
-          Tn.put(j, cmul(tp, cconj(u[W])));
+          const double2 t = cmul(tp, cconj(u[W]));
+          Tn.put(j, t);
 #pragma unroll
           for (int d = 1; d <= W; d++) acc[d - 1] = cfms_cj(acc[d], u[d - 1], tp);
           acc[W] = czero();
+          return isfinite(t.x) && isfinite(t.y);
         });
       }
       if (!ok) {

@@ -32,27 +32,44 @@ constexpr int MLP_TPB = 32;  // threads per block (one warp): smem = 3 * 128 * 3
 __device__ __forceinline__ double expit_d(double x) { return 1.0 / (1.0 + exp(-x)); }
 
 // numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src pairwise_sum, PW_BLOCKSIZE 128)
-// over f(k), k in [lo, lo+len)
+// over f(k), k in [lo, lo+len). Blocks of <= 128 terms: 8 running sums, combined as a tree.
 template <class F>
-__device__ double np_pairwise(F f, int lo, int len) {
+__device__ double np_pairwise_leaf(F f, int lo, int len) {
   if (len < 8) {
     double res = 0.0;  // numpy starts from -0.0 for sums; identical for the non-negative terms here
     for (int i = 0; i < len; i++) res += f(lo + i);
     return res;
-  } else if (len <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; j++) r[j] = f(lo + j);
-    int i;
-    for (i = 8; i < len - (len % 8); i += 8)
-      for (int j = 0; j < 8; j++) r[j] += f(lo + i + j);
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < len; i++) res += f(lo + i);
-    return res;
-  } else {
-    int n2 = len / 2;
-    n2 -= n2 % 8;
-    return np_pairwise(f, lo, n2) + np_pairwise(f, lo + n2, len - n2);
   }
+  double r[8];
+  for (int j = 0; j < 8; j++) r[j] = f(lo + j);
+  int i;
+  for (i = 8; i < len - (len % 8); i += 8)
+    for (int j = 0; j < 8; j++) r[j] += f(lo + i + j);
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < len; i++) res += f(lo + i);
+  return res;
+}
+
+// numpy's recursion (len > 128: split at n2 = len/2 rounded down to a multiple of 8, left + right)
+// evaluated in post-order on an explicit stack: device recursion would live on the per-thread call
+// stack (1 KB by default), which n = 2000 eigenvalues (five levels) overflowed.
+template <class F>
+__device__ double np_pairwise(F f, int lo, int len) {
+  struct Frame { int lo, len, state; double left; };
+  Frame st[32];  // depth <= log2(2^31 / 128) + 1
+  int sp = 0;
+  st[0] = Frame{lo, len, 0, 0.0};
+  double ret = 0.0;
+  while (sp >= 0) {
+    Frame& fr = st[sp];
+    if (fr.len <= 128) { ret = np_pairwise_leaf(f, fr.lo, fr.len); sp--; continue; }
+    int n2 = fr.len / 2;
+    n2 -= n2 % 8;
+    if (fr.state == 0) { fr.state = 1; st[sp + 1] = Frame{fr.lo, n2, 0, 0.0}; sp++; }
+    else if (fr.state == 1) { fr.left = ret; fr.state = 2; st[sp + 1] = Frame{fr.lo + n2, fr.len - n2, 0, 0.0}; sp++; }
+    else { ret = fr.left + ret; sp--; }
+  }
+  return ret;
 }
 
 __device__ __forceinline__ void dense(const double* __restrict__ W, const double* __restrict__ bvec, int nin,

@@ -52,6 +52,38 @@ def test_hierarchical_and_region_match_reference(gpu, gold, bundle, name, cfg):
     assert region.mean() == pytest.approx(float(z["region"].mean()), abs=1e-3)
 
 
+def test_c4_guided_matches_reference(gpu, gold):
+    """BASELINE configs[3] guided path: the reference's hierarchical_predict / predicted_region on the C4
+    512 x 512 grid with a bundle it trained and calibrated on a convection-diffusion family
+    (oracle/make_guided_c4.py). The per-matrix features come from the fixture (host LAPACK bits of an
+    n=2000 non-normal eig vary between CPUs); n_eig = 2000 exercises K2's pairwise sums at depth 5."""
+    if not (GOLD / "c4_guided.npz").exists():
+        pytest.skip("c4_guided.npz not generated")
+    z = gold("c4_guided.npz")
+    b4 = pipeline.load_npz(GOLD / "model_c4.npz")
+    S = float(z["scale"])  # exact power-of-two units (make_guided_c4.py): sigma(SzI - SA) = S sigma(zI - A)
+    A4 = configs.CONFIGS["C4"].matrix()
+    A = core.BandMatrix(A4.band * S, A4.kl, A4.ku)
+    grid = core.make_grid(*(v * S for v in configs.C4_BOX), 512, 512)
+    gf = pipeline.GlobalFeatures(values=z["f30"], eigvals=z["eig"], singvals=np.zeros(0))
+    prob, n_evals = pipeline.hierarchical_predict(b4, None, grid, stride=4, gf=gf)
+    assert n_evals == int(z["n_evals"])
+    assert np.max(np.abs(prob - z["prob"])) <= PTOL
+    region = pipeline.predicted_region(prob, b4.tau_star)
+    near = np.abs(z["prob"] - b4.tau_star) <= PTOL
+    diff = region != z["region"]
+    if diff.any():
+        assert np.all(core.dilate(near, 5)[diff])
+    # the restricted sweep on that region equals the full map there (restriction exactness), and the
+    # full map in these units is the C4 map times S
+    got = core._selection_call(A, grid, region, "C4")
+    full = core.full_pseudospectrum(A, grid).values
+    assert np.array_equal(got[region], full[region])
+    orig = core.full_pseudospectrum(A4, configs.CONFIGS["C4"].grid).values
+    assert np.max(np.abs(full - S * orig) / np.maximum(S * orig, 1e-5 * S * 1.6e7)) <= 1e-9
+    print(f"\n[guided] C4: region fraction {region.mean():.3f}, n_evals {n_evals}")
+
+
 def test_hybrid_restriction_exactness(gpu, bundle):
     """tests/test_acceptance.py:145-157: hybrid field == full field on the region, bitwise."""
     c = configs.CONFIGS["C2"]

@@ -1,6 +1,7 @@
 """A/B two library builds on full σ maps (development tool): bitwise equality and per-matrix kernel times.
 
 Usage: python tools/ab_maps.py C5 0,1,17,63 ablib/libpsb200_base.so paper_2605_04550_b200/libpsb200.so
+A side may carry environment knobs: lib.so@PSB_SEQ=1,PSB_TAU=2e-3
 """
 import json
 import os
@@ -30,9 +31,11 @@ for m in [int(x) for x in sys.argv[2].split(',')]:
 print(json.dumps(out))
 """
 res = {}
-for tag, lib in (("a", la), ("b", lb)):
+for tag, spec in (("a", la), ("b", lb)):
+    lib, _, knobs = spec.partition("@")
+    extra = dict(kv.split("=", 1) for kv in knobs.split(",") if kv)
     r = subprocess.run([sys.executable, "-c", code, name, sys.argv[2], tag], capture_output=True, text=True,
-                       env={**os.environ, "PSB200_LIB": lib})
+                       env={**os.environ, "PSB200_LIB": lib, **extra})
     if r.returncode:
         print(r.stderr[-3000:])
         sys.exit(1)
