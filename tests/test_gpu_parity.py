@@ -70,6 +70,31 @@ def test_c5_sample(gpu, gold):
         check(got, z["sigma"][r], float(z["norm2"][r]), f"C5[{m}]")
 
 
+def test_c5_stratified(gpu, gold):
+    """C5 pinned on meaningful points (oracle/make_golden.py gen_c5_strat): 4 of the 64 matrices x 64 grid
+    shifts chosen from full C5 maps by what they exercise - general-band bisection points above the parity
+    floor, points straddling the engine split, points within 20% of an eps level, Lanczos points above
+    the floor - each against the restated zgesdd. Every engine must be pinned on many of them."""
+    z = gold("c5_strat.npz")
+    cfg = configs.CONFIGS["C5"]
+    worst, above, by_engine = 0.0, 0, {0: 0, 1: 0}
+    for r, m in enumerate(z["matrices"]):
+        A = cfg.matrix(int(m))
+        want = z["sigma"][r]
+        n2 = float(z["norm2"][r])
+        got, it, st = core.smin_many(A, z["zs"][r], return_info=True)
+        worst = max(worst, check(got, want, n2, f"C5 strat[{m}]"))
+        live = want >= 1e-5 * n2
+        above += int(live.sum())
+        for e in (0, 1):
+            by_engine[e] += int((live & (st == e)).sum())
+        masks_agree(got, want, n2, [1e-1, 1e-2, 1e-3])
+    print(f"\n[parity] C5 stratified: {above} points above the floor (engine L {by_engine[0]}, engine B "
+          f"{by_engine[1]}), worst floored rel err {worst:.3g} (gate {TOL})")
+    assert above >= 64 * len(z["matrices"]) - 8
+    assert by_engine[1] >= 64 and by_engine[0] >= 32
+
+
 def test_small_random_reference_acceptance_form(gpu, gold):
     """tests/test_acceptance.py:53-70: |got - want| / max(1, want) < 1e-10 over random banded A."""
     z = gold("small_random.npz")
