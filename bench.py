@@ -166,36 +166,37 @@ def _dense(cfg, m=0):
 
 
 def _oracle_chunk(args):
-    A, zs = args
+    A, zs, threads = args
     from oracle.sigma_oracle import smin_restated
-    return smin_restated(A, zs)
+    return smin_restated(A, zs, threads=threads)
 
 
 def _reference_chunk(args):
-    """The reference package's own smin_many (baseline/_ref, stock code path; real A only)."""
-    A, zs = args
+    """The reference package's own smin_many (baseline/_ref, stock code path; real A only). BLAS threads are
+    set explicitly: forked pool children inherit the parent's initialised OpenBLAS, so OPENBLAS_NUM_THREADS
+    set after numpy's import would not reach them (SURVEY §0.6's 8 x 8 oversubscription)."""
+    A, zs, threads = args
     sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+    from threadpoolctl import threadpool_limits
+
     from pseudospec import core as rcore
-    return rcore.smin_many(A, zs, chunk=1)
+    with threadpool_limits(threads):
+        return rcore.smin_many(A, zs, chunk=1)
 
 
 def _reference_available() -> bool:
     return (ROOT / "baseline" / "_ref" / "pseudospec" / "core.py").exists()
 
 
-def cpu_rate(fn, A_dense, zs, procs: int, blas_threads: int) -> tuple[float, float]:
-    """pts/s of `fn` over zs: `procs` processes (each OPENBLAS `blas_threads`) or in-process."""
-    from threadpoolctl import threadpool_limits
+def cpu_rate(fn, A_dense, zs, procs: int, blas_threads: int, pool=None) -> tuple[float, float]:
+    """pts/s of `fn` over zs: on `pool` (a process pool of `procs` workers, each with `blas_threads` BLAS
+    threads) or in-process."""
     t0 = time.perf_counter()
-    if procs <= 1:
-        with threadpool_limits(blas_threads):
-            fn((A_dense, zs))
+    if procs <= 1 or pool is None:
+        fn((A_dense, zs, blas_threads))
     else:
-        from concurrent.futures import ProcessPoolExecutor
-        os.environ["OPENBLAS_NUM_THREADS"] = str(blas_threads)
         chunks = [c for c in np.array_split(zs, procs) if c.size]
-        with ProcessPoolExecutor(max_workers=procs) as ex:
-            list(ex.map(fn, [(A_dense, c) for c in chunks]))
+        list(pool.map(fn, [(A_dense, c, blas_threads) for c in chunks]))
     dt = time.perf_counter() - t0
     return zs.size / dt, dt
 
@@ -220,14 +221,22 @@ def run_reference(args, rank, world):
         per_step, procs, blas = {"C1": 40, "C2": 4, "C3": 1, "C4": 1}[args.config] * cores, cores, 1
     rng = np.random.default_rng(7)
     pts = cfg.grid.points().ravel()
-    for _ in range(args.warmup):
-        cpu_rate(fn, A, pts[rng.choice(pts.size, per_step, replace=False)], procs, blas)
+    pool = None
+    if procs > 1:  # one pool for the whole run (worker start-up and imports stay out of the steps)
+        from concurrent.futures import ProcessPoolExecutor
+        pool = ProcessPoolExecutor(max_workers=procs)
     times, npts = [], 0
-    for _ in range(args.steps):
-        zs = pts[rng.choice(pts.size, per_step, replace=False)]
-        _, dt = cpu_rate(fn, A, zs, procs, blas)
-        times.append(dt)
-        npts += zs.size
+    try:
+        for _ in range(args.warmup):
+            cpu_rate(fn, A, pts[rng.choice(pts.size, per_step, replace=False)], procs, blas, pool)
+        for _ in range(args.steps):
+            zs = pts[rng.choice(pts.size, per_step, replace=False)]
+            _, dt = cpu_rate(fn, A, zs, procs, blas, pool)
+            times.append(dt)
+            npts += zs.size
+    finally:
+        if pool is not None:
+            pool.shutdown()
     value = npts / sum(times)
     how = (f"{per_step} random grid shift(s) per step of the {args.config} grid, "
            + ("pseudospec.core.smin_many (baseline/_ref, unmodified)" if kind == "reference"
@@ -382,7 +391,10 @@ def run_ours(args, rank, world, local_rank):
     gather_in = torch.full((m_pad,), float("nan"), dtype=torch.float64, device=dev) if (world > 1 and not batch) else None
     gathered = torch.empty(world * m_pad, dtype=torch.float64, device=dev) if gather_in is not None else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream (not the legacy default one, whose handle is 0 and would make the library fall back
+    # to its own unordered stream): the L2 flush, the step's kernels and the timing events are then ordered
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     used = []
 
     def prepare(step):  # outside the timed region: the step's matrix resident on the device

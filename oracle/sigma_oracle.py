@@ -18,15 +18,16 @@ import numpy as np
 from threadpoolctl import threadpool_limits
 
 
-def smin_restated(A, zs, chunk: int = 1) -> np.ndarray:
-    """σ_min(z I - A) for every z in zs (core.py:141-168 without the real cast)."""
+def smin_restated(A, zs, chunk: int = 1, threads: int = 1) -> np.ndarray:
+    """σ_min(z I - A) for every z in zs (core.py:141-168 without the real cast). BLAS runs on `threads`
+    threads (1 by default: the fixtures' bits; the reference's protocol is single-thread)."""
     A = np.asarray(A)
     A = A.astype(complex if np.iscomplexobj(A) else float)
     zs = np.asarray(zs, dtype=complex).ravel()
     n = A.shape[0]
     eye = np.eye(n)
     out = np.empty(zs.size)
-    with threadpool_limits(1):
+    with threadpool_limits(threads):
         for start in range(0, zs.size, chunk):
             zc = zs[start:start + chunk]
             shifted = zc[:, None, None] * eye - A

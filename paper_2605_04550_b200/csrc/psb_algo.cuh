@@ -133,6 +133,13 @@ struct NoRowHook {
   PSB_HD bool operator()(int, const double2 (&)[N]) const { return true; }
 };
 
+// LU row loop unroll: 1 (measured against 2: C5 -2..4%, C2/C4 unchanged; half the code of the kernel's
+// hottest loop, whose warps also walk four sweep loops per pass - ncu put 25% of engine L's stall samples
+// on instruction fetch at 2)
+#ifndef PSB_LU_UNROLL
+#define PSB_LU_UNROLL 1
+#endif
+constexpr int kLuUnroll = PSB_LU_UNROLL;
 // `hook(j, u)` sees each finished U row (u[0..W-1] = U', u[W] = rinv) in forward order, so a
 // forward sweep that needs exactly these rows can run fused with the factorization. A hook that
 // returns false ends the factorization there (lu_factor returns false, as for an exact zero pivot).
@@ -166,7 +173,7 @@ PSB_HD bool lu_factor(const Shape& s, const double2* __restrict__ Ab, double2 z,
   double2 pre[WM + 1];
 #pragma unroll
   for (int c = 0; c <= WM; c++) pre[c] = (c <= W && kl + 1 < n) ? Ab[(int64_t)c * n + kl + 1] : czero();
-#pragma unroll 2
+#pragma unroll kLuUnroll
   for (int j = 0; j < n; j++) {
     // pivot among rows j..j+kl (rows past n are zero and never win a strict '>')
     int p = 0;
