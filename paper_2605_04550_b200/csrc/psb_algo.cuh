@@ -20,8 +20,8 @@
 //     eps/tau^2 relative accuracy, and Toeplitz-like continua of singular values
 //     (which stall Lanczos) do not slow bisection.
 //
-// Every function here is __host__ __device__ so the identical arithmetic can be
-// exercised on the host by tools/algo_mirror.cu (a test tool, never a product path).
+// Every function here is __host__ __device__, so the same arithmetic also compiles for the host
+// (the runtime-shape and static-shape paths share it; only device code calls it in the product).
 #pragma once
 #include <stdint.h>
 #include <math.h>
