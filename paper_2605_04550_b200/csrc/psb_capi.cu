@@ -79,6 +79,7 @@ struct psb_handle {
   //   Lanczos warps, PSB_PROF=1 per-phase clock64 counters of the Lanczos kernel (stderr)
   bool k_secant = true, k_toeplitz = true, k_prof = false;
   long long k_lwarps = 0;
+  int k_refill = 16;
   int k_btpb = 128;
   double k_tau = 0.0;
   bool k_bexpand = true, k_fallback = true, k_seq = false;
@@ -193,6 +194,7 @@ int psb_create(int device, psb_handle** out) {
   h->k_tau = getenv("PSB_TAU") ? atof(getenv("PSB_TAU")) : 0.0;  // dev: default engine split
   h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 0;  // 0: pick per launch
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
+  h->k_refill = getenv("PSB_REFILL") ? atoi(getenv("PSB_REFILL")) : 16;  // dev: engine-L refill threshold
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
@@ -413,7 +415,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   // A function of the matrix only, so every sigma stays a function of (A, z). Measured per config:
   // n >= 1000 (C3-C5) is faster at 1e-3 (C4 102 -> 85 ms); at n = 400 (C2) 1e-3 leaves the
   // bisection engine a few more points than it has threads next to engine L (2.2 -> 2.46 ms).
-  opt.tau = h->k_tau > 0 ? h->k_tau : (h->n >= 1000 ? 1e-3 : 1.5e-3); opt.bis_rtol = 2e-12; opt.kmax = 0; opt.force_engine = 0; opt.refill = 16;
+  opt.tau = h->k_tau > 0 ? h->k_tau : (h->n >= 1000 ? 1e-3 : 1.5e-3); opt.bis_rtol = 2e-12; opt.kmax = 0; opt.force_engine = 0; opt.refill = h->k_refill;
   if (o) {
     if (o->tau > 0) opt.tau = o->tau;
     if (o->bis_rtol > 0) opt.bis_rtol = o->bis_rtol;

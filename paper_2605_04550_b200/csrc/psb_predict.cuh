@@ -72,10 +72,29 @@ __device__ double np_pairwise(F f, int lo, int len) {
   return ret;
 }
 
+// y[o] = act(b[o] + sum_i W[o, i] x[i]): four outputs per pass, so four independent FMA chains are in
+// flight (one chain per output was latency-bound at two warps per SM); each output keeps its own
+// sequential sum order, so the values do not change.
 __device__ __forceinline__ void dense(const double* __restrict__ W, const double* __restrict__ bvec, int nin,
                                       int nout, const double* x, double* y, bool act) {
   const int t = threadIdx.x;
-  for (int o = 0; o < nout; o++) {
+  int o = 0;
+  for (; o + 4 <= nout; o += 4) {
+    const double* w = W + (int64_t)o * nin;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int i = 0; i < nin; i++) {
+      const double xi = x[i * MLP_TPB + t];
+      a0 = fma(__ldg(w + i), xi, a0);
+      a1 = fma(__ldg(w + nin + i), xi, a1);
+      a2 = fma(__ldg(w + 2 * nin + i), xi, a2);
+      a3 = fma(__ldg(w + 3 * nin + i), xi, a3);
+    }
+    const double acc[4] = {a0 + __ldg(bvec + o), a1 + __ldg(bvec + o + 1), a2 + __ldg(bvec + o + 2),
+                           a3 + __ldg(bvec + o + 3)};
+#pragma unroll
+    for (int k = 0; k < 4; k++) y[(o + k) * MLP_TPB + t] = act ? acc[k] * expit_d(acc[k]) : acc[k];
+  }
+  for (; o < nout; o++) {
     const double* w = W + (int64_t)o * nin;
     double acc = 0.0;
     for (int i = 0; i < nin; i++) acc = fma(__ldg(w + i), x[i * MLP_TPB + t], acc);

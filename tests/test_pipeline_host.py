@@ -95,3 +95,18 @@ def test_fine_points_match_reference_enumeration():
                 if (r, c) != (ay[iy], ax[ix]):
                     want.append((r, c))
     assert list(zip(rows.tolist(), cols.tolist())) == want
+
+
+def test_fine_points_vectorised_order():
+    """The vectorised fine-point list equals the per-cell loop (pipeline.py:206-215 order), clipped cells too."""
+    import numpy as np
+
+    from paper_2605_04550_b200 import pipeline
+    rng = np.random.default_rng(3)
+    for ny, nx, s in ((50, 50, 4), (37, 53, 4), (512, 512, 4), (9, 7, 3), (5, 5, 4)):
+        ay, ax = np.arange(0, ny, s), np.arange(0, nx, s)
+        for frac in (0.0, 0.2, 1.0):
+            flagged = rng.random((ay.size, ax.size)) < frac
+            a = pipeline._fine_points(flagged, ay, ax, s, ny, nx)
+            b = pipeline._fine_points_loop(flagged, ay, ax, s, ny, nx)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
