@@ -6,6 +6,8 @@ import subprocess
 import sys
 from pathlib import Path
 
+import pytest
+
 ROOT = Path(__file__).resolve().parent.parent
 
 
@@ -30,3 +32,19 @@ def test_reference_arm_line():
     assert line["impl"] == "reference" and line["unit"] == "points/s" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["cores"] >= 1
     assert line["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+@pytest.mark.gpu
+def test_bench_line_on_gpu():
+    """One short C1 bench run on the GPU: a well-formed line whose dominant kernel window fits inside the step
+    (the events bracket each launch on its own stream), with the library's own launch count."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--config", "C1", "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline", "--no-guided"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    (line,) = _json_lines(r.stdout)
+    assert line["metric"].startswith("sigma_min") and line["value"] > 0 and line["n_gpus"] == 1
+    roof = line["roofline"]
+    assert 0 < roof["share_of_step"] <= 1.001 and roof["frac"] > 0
+    assert line["gpu_launches"] >= 3 * 2
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert line["engines"]["lanczos_points"] + line["engines"]["bisect_points"] == 2500
