@@ -89,7 +89,7 @@ struct psb_handle {
   struct LanEntry { const void* f; int lsmem, occ, regs; };
   std::vector<LanEntry> lan_cache;  // engine-L occupancy and registers per kernel
   bool have_matrix = false;
-  DevBuf Ab, AHA, RT, v1, offmin, gbuf, listF;
+  DevBuf Ab, AHA, RT, LUT, v1, offmin, gbuf, listF;
   // per call
   DevBuf zs, outidx, out, iters, status, listA, listB, counters, scratch, pivs, dynL, dynD;
   DevBuf xs, ys, prof;
@@ -205,7 +205,7 @@ int psb_create(int device, psb_handle** out) {
 void psb_destroy(psb_handle* h) {
   if (!h) return;
   DeviceGuard dg(h->device);
-  DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->RT, &h->v1, &h->offmin, &h->gbuf, &h->listF, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
+  DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->RT, &h->LUT, &h->v1, &h->offmin, &h->gbuf, &h->listF, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
                     &h->counters, &h->scratch, &h->pivs, &h->dynL, &h->dynD, &h->xs, &h->ys, &h->params,
                     &h->feat, &h->eig, &h->prob, &h->region, &h->idx, &h->selblk};
   for (DevBuf* b : bufs) b->release();
@@ -350,6 +350,18 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
     for (int l = 0; l < 32; l++) v1x[(size_t)n + (size_t)i * 32 + l] = v1[i];
   }
   CK(cudaMemcpyAsync(h->v1.p, v1x.data(), sizeof(cd) * n * 33, cudaMemcpyHostToDevice, h->stream));
+  // the staged LU's row stream (LUS, psb_engines.cuh): row j = [A[j+1+kl, j+1+c] for c = 0..b (0 outside the
+  // matrix) | v1[j]]
+  std::vector<cd> lut((size_t)(b + 2) * n, cd(0, 0));
+  for (int j = 0; j < n; j++) {
+    cd* row = lut.data() + (size_t)j * (b + 2);
+    const int i = j + 1 + kl;
+    for (int c = 0; c <= b; c++)
+      if (i < n && j + 1 + c < n) row[c] = A[(int64_t)c * n + i];
+    row[b + 1] = v1[j];
+  }
+  CK(h->LUT.ensure(sizeof(cd) * lut.size()));
+  CK(cudaMemcpyAsync(h->LUT.p, lut.data(), sizeof(cd) * lut.size(), cudaMemcpyHostToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   h->n = n; h->kl = kl; h->ku = ku;
   // Rows whose G(lambda) row entries are bitwise identical: G row j is formed from A's rows
@@ -535,6 +547,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     la.s = s; la.Ab = h->Ab.as<double2>();
     la.v1 = dyn ? h->v1.as<double2>() : h->v1.as<double2>() + n;  // pipelined sweeps read the replicated copy
     la.v1b = h->v1.as<double2>();
+    la.LUT = h->LUT.as<double2>();
     la.zs = d_zs; la.outidx = d_outidx; la.listA = h->listA.as<int64_t>(); la.counters = cnt; la.listF = h->listF.as<int64_t>();
     la.zscale = h->zscale; la.sscale = h->sscale;
     la.out = d_out; la.iters = d_iters; la.status = d_status;

@@ -16,7 +16,7 @@ typedef void (*lan_fn)(LanArgs);
 // bm2 / bmt2: the pair variant, the same K = 2 probes per round on two lanes (NP = 1, G = 2). Both
 // variants test the same shifts with the same arithmetic, so they return the same bits and the host
 // may pick either per launch (the pair for short lists, where each thread holds about one point).
-// np, g: the wide variant's split. lsmem: Lanczos ring bytes per warp. kl = -1: runtime-shape set.
+// np, g: the wide variant's split. lsmem: engine-L shared memory per warp (sweep ring + LU stage). kl = -1: runtime-shape set.
 // bsmem: shared-memory row stages per warp of the general-band (non-TZ) bisection kernels (BisRow).
 struct KPair { int kl, ku; bis_fn b, bm, bt, bmt, bm2, bmt2; lan_fn l; int lsmem; int np, g; int bsmem; };
 

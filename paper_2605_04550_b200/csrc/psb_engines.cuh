@@ -64,6 +64,7 @@ struct LanArgs {
   const double2* __restrict__ Ab;
   const double2* __restrict__ v1;
   const double2* __restrict__ v1b;  // v1 once (n entries): warp-uniform loads in the fused LU + S1
+  const double2* __restrict__ LUT;  // static shapes: the staged LU's row stream (LUS, psb_set_matrix)
   const double2* __restrict__ zs;
   const int64_t* __restrict__ outidx;
   const int64_t* __restrict__ listA;
@@ -766,6 +767,150 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   }
 }
 
+// ----------------------------------------------------------------- engine L: staged LU
+// Row stream of the staged factorization (psb_set_matrix, static shapes): row j holds what LU step j
+// reads besides its window, [A[j+1+kl, j+1+c] for c = 0..W (0 outside the matrix) | v1[j]], W + 2 complex.
+template <int KL, int KU>
+struct LUS {
+  static constexpr int W = KL + KU;
+  static constexpr int RW = W + 2;
+  static constexpr int RB = 8;             // rows per stage
+  static constexpr int SE = RB * RW;       // complex per stage
+  static constexpr int BYTES = 2 * SE * 16;  // two stages per warp
+};
+
+// Band LU of M = zI - A fused with S1 of Lanczos step 1 (t = U^{-H} v1), warp-uniform: every lane runs the
+// row loop in lockstep - lanes without a point in the LU phase (live = false), or whose point is already
+// decided, compute on and store nothing - so the z-independent row stream can be staged per warp in shared
+// memory by all 32 lanes with cp.async, one 8-row block ahead. (lu_factor loads the next band row and v1
+// entry one row ahead per lane; the copy of those loads into the window then waited on L2 every row: ncu
+// put 40% of engine L's stall samples on long-scoreboard on C5.) The arithmetic is lu_factor's with the
+// fused hook, operation for operation, so the factors, T, R and the outcome carry the same bits. A point is
+// decided by an exact zero pivot or a non-finite t_j (see the caller): both finish it as singular (status 2).
+template <int KL, int KU>
+__device__ bool lu_staged(int n, const double2* __restrict__ Ab, const double2* __restrict__ LUT, double2* stg,
+                          int lane, bool live, double2 z, LV FU, LV FL, LVb piv, LV Tn, LV Rn) {
+  constexpr int W = KL + KU, NU = W + 1, NL = (KL > 0 ? KL : 1);
+  typedef LUS<KL, KU> SS;
+  const unsigned FULL = 0xffffffffu;
+  bool ok = live;
+  double2 win[KL + 1][W + 1];
+#pragma unroll
+  for (int r = 0; r <= KL; r++) {
+#pragma unroll
+    for (int c = 0; c <= W; c++) {
+      double2 v = czero();
+      if (r < n && c < n) {
+        const int d = c - r;
+        if (d >= -KL && d <= KU) {
+          const double2 a = Ab[(int64_t)(d + KL) * n + r];
+          v = cmk((d == 0 ? z.x : 0.0) - a.x, (d == 0 ? z.y : 0.0) - a.y);
+        }
+      }
+      win[r][c] = v;
+    }
+  }
+  double2 acc[W + 1];
+#pragma unroll
+  for (int d = 0; d <= W; d++) acc[d] = czero();
+  auto fill = [&](int sidx, int j0) {
+    double2* dst = stg + sidx * SS::SE;
+#pragma unroll
+    for (int e0 = 0; e0 < SS::SE; e0 += 32) {
+      const int e = e0 + lane;
+      if (e0 + 32 <= SS::SE || e < SS::SE) {
+        const int row = j0 + e / SS::RW;
+        cp16z(dst + e, LUT + (int64_t)(row < n ? row : n - 1) * SS::RW + (e % SS::RW), row < n ? 16u : 0u);
+      }
+    }
+    cp_commit();
+  };
+  int sidx = 0;
+  fill(0, 0);
+  for (int j0 = 0; j0 < n; j0 += SS::RB) {
+    if (!__any_sync(FULL, ok)) break;  // every point of the warp decided
+    fill(sidx ^ 1, j0 + SS::RB);
+    cp_wait<1>();
+    __syncwarp();
+    const double2* st = stg + sidx * SS::SE;
+#pragma unroll 1
+    for (int q = 0; q < SS::RB; q++) {
+      const int j = j0 + q;
+      if (j >= n) break;
+      const double2* row = st + q * SS::RW;
+      int p = 0;
+      double best = cabs1(win[0][0]);
+#pragma unroll
+      for (int r = 1; r <= KL; r++) {
+        const double m = cabs1(win[r][0]);
+        if (m > best) { best = m; p = r; }
+      }
+#pragma unroll
+      for (int r = 1; r <= KL; r++) {
+        if (p == r) {
+#pragma unroll
+          for (int c = 0; c <= W; c++) { const double2 t = win[0][c]; win[0][c] = win[r][c]; win[r][c] = t; }
+        }
+      }
+      if (ok) piv.put(j, p);
+      const double2 d = win[0][0];
+      double2 ri;
+      if (d.x == 0.0 && d.y == 0.0) { ok = false; ri = czero(); }
+      else ri = crcp_fast(d);
+      const int64_t rb = (int64_t)j * NU;
+      double2 u[W + 1];
+#pragma unroll
+      for (int c = 1; c <= W; c++) {
+        u[c - 1] = cmul(win[0][c], ri);
+        if (ok) FU.put(rb + c - 1, u[c - 1]);
+      }
+      u[W] = ri;
+      if (ok) FU.put(rb + W, ri);
+      // fused S1 at k = 1 (the lu_factor hook): r = v1[j], t_j = (r + acc_0) conj(rinv_j)
+      {
+        const double2 r = row[W + 1];
+        if (ok) Rn.put(j, r);
+        const double2 tp = cadd(r, acc[0]);
+        const double2 t = cmul(tp, cconj(u[W]));
+        if (ok) Tn.put(j, t);
+#pragma unroll
+        for (int dd = 1; dd <= W; dd++) acc[dd - 1] = cfms_cj(acc[dd], u[dd - 1], tp);
+        acc[W] = czero();
+        if (!(isfinite(t.x) && isfinite(t.y))) ok = false;
+      }
+#pragma unroll
+      for (int r = 1; r <= KL; r++) {
+        const double2 l = cmul(win[r][0], ri);
+        if (ok) FL.put((int64_t)j * NL + r - 1, l);
+#pragma unroll
+        for (int c = 1; c <= W; c++) win[r][c] = cfms(win[r][c], l, win[0][c]);
+      }
+#pragma unroll
+      for (int r = 0; r < KL; r++) {
+#pragma unroll
+        for (int c = 0; c < W; c++) win[r][c] = win[r + 1][c + 1];
+        win[r][W] = czero();
+      }
+      // new bottom row: matrix row i = j+1+kl, columns j+1 .. j+1+W, from the stage (lu_factor's `pre`)
+      const int i = j + 1 + KL;
+#pragma unroll
+      for (int c = 0; c <= W; c++) {
+        double2 v = czero();
+        if (i < n && j + 1 + c < n) {
+          const double2 a = row[c];
+          v = cmk((c == KL ? z.x : 0.0) - a.x, (c == KL ? z.y : 0.0) - a.y);
+        }
+        win[KL][c] = v;
+      }
+    }
+    __syncwarp();  // every lane has read stage sidx before the next block refills it
+    sidx ^= 1;
+  }
+  cp_wait<0>();
+  __syncwarp();
+  return ok;
+}
+
 // ----------------------------------------------------------------- engine L kernel
 template <int KL, int KU, bool DYN, int DPIPE>
 __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
@@ -788,10 +933,13 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
   typedef Ring<(KL > 0 ? KL : 1), KU, DPIPE> RG;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RG ring;
+  double2* lstage = nullptr;
   if constexpr (!DYN) {
     const int wib = threadIdx.x >> 5;
-    ring.d = reinterpret_cast<double2*>(smem_raw + (size_t)wib * RG::BYTES);
-    ring.pv = reinterpret_cast<int*>(smem_raw + (size_t)wib * RG::BYTES + DPIPE * RG::SF * 32 * 16);
+    constexpr size_t kWarpSmem = RG::BYTES + LUS<(KL > 0 ? KL : 1), KU>::BYTES;  // ring | LU stage
+    ring.d = reinterpret_cast<double2*>(smem_raw + (size_t)wib * kWarpSmem);
+    ring.pv = reinterpret_cast<int*>(smem_raw + (size_t)wib * kWarpSmem + DPIPE * RG::SF * 32 * 16);
+    lstage = reinterpret_cast<double2*>(smem_raw + (size_t)wib * kWarpSmem + RG::BYTES);
     ring.lane = lane;
   }
   const int64_t nA = (int64_t)a.counters[1];
@@ -833,43 +981,31 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       if ((int64_t)bq + nidle >= nA) exhausted = true;
     }
     long long tq0 = clock64();
-    if (phase == 1) {
-      bool ok;
-      if constexpr (DYN) {
-        ok = lu_factor<KL, KU, DYN>(s, a.Ab, z, FU, FL, piv);
-      } else {
-        // LU fused with S1 of step 1 (t = U^{-H} v1): the same arithmetic as pl_s1 at k = 1
-        // (r = v1 exactly), on the U rows as the factorization produces them
-        constexpr int W = KL + KU;
-        const LV Tn = T, Rn = rsw ? RA0 : RB0;  // pl_s1 writes r into the current RB, then swaps
-        double2 acc[W + 1];
-#pragma unroll
-        for (int d = 0; d <= W; d++) acc[d] = czero();
-        const double2* __restrict__ v1b = a.v1b;
-        double2 vnext = v1b[0];  // one row ahead
-        // A non-finite t_j = (U^{-H} v1)_j decides the point already: S2 would carry it into
-        // nu = ||M^{-H} v1|| (every T entry reaches nu's sum), and a non-finite nu finishes the point as
-        // singular to working precision (sigma = 0, status 2) - the outcome of an exact zero pivot. So
-        // the factorization stops at that row (the same results; deep inside the pseudospectrum of a
-        // strongly non-normal band, U^{-H} v1 overflows a few hundred rows in, C5).
-        ok = lu_factor<KL, KU, DYN>(s, a.Ab, z, FU, FL, piv, [&](int j, const double2 (&u)[W + 1]) {
-          const double2 r = vnext;
-          if (j + 1 < n) vnext = v1b[j + 1];
-          Rn.put(j, r);
-          const double2 tp = cadd(r, acc[0]);
-          const double2 t = cmul(tp, cconj(u[W]));
-          Tn.put(j, t);
-#pragma unroll
-          for (int d = 1; d <= W; d++) acc[d - 1] = cfms_cj(acc[d], u[d - 1], tp);
-          acc[W] = czero();
-          return isfinite(t.x) && isfinite(t.y);
-        });
+    if constexpr (DYN) {
+      if (phase == 1) {
+        const bool ok = lu_factor<KL, KU, DYN>(s, a.Ab, z, FU, FL, piv);
+        if (!ok) finish(0.0, 0, 2);
+        else { phase = 2; k = 1; nu = 1.0; b1 = 1.0; b2 = 1.0; aprev = 0.0; theta = 0.0; s2 = 1.0; dth = 0.0; }
       }
-      if (!ok) {
-        finish(0.0, 0, 2);
-      } else {
-        phase = 2; k = 1; nu = 1.0; b1 = 1.0; b2 = 1.0; aprev = 0.0; theta = 0.0; s2 = 1.0; dth = 0.0;
-        if constexpr (!DYN) { s1done = true; rsw = !rsw; }
+    } else if (__any_sync(FULL, phase == 1)) {
+      // LU fused with S1 of step 1 (t = U^{-H} v1): the same arithmetic as pl_s1 at k = 1 (r = v1 exactly),
+      // on the U rows as the factorization produces them; the whole warp runs it (lu_staged).
+      // A non-finite t_j decides the point already: S2 would carry it into nu = ||M^{-H} v1|| (every T entry
+      // reaches nu's sum), and a non-finite nu finishes the point as singular to working precision
+      // (sigma = 0, status 2) - the outcome of an exact zero pivot. So the point's factorization stops
+      // there (the same results; deep inside the pseudospectrum of a strongly non-normal band U^{-H} v1
+      // overflows a few hundred rows in, C5).
+      const bool mine = phase == 1;
+      const LV Tn = T, Rn = rsw ? RA0 : RB0;  // pl_s1 writes r into the current RB, then swaps
+      const bool ok = lu_staged<(KL > 0 ? KL : 1), KU>(n, a.Ab, a.LUT, lstage, lane, mine, mine ? z : czero(),
+                                                       FU, FL, piv, Tn, Rn);
+      if (mine) {
+        if (!ok) {
+          finish(0.0, 0, 2);
+        } else {
+          phase = 2; k = 1; nu = 1.0; b1 = 1.0; b2 = 1.0; aprev = 0.0; theta = 0.0; s2 = 1.0; dth = 0.0;
+          s1done = true; rsw = !rsw;
+        }
       }
     }
     long long tq1 = clock64();

@@ -20,7 +20,8 @@ const KPair kSet = {PSB_KL, PSB_KU, &k_bisect<PSB_KL, PSB_KU, false, 1, 1, false
                     &k_bisect<PSB_KL, PSB_KU, false, PSB_NP, PSB_G, true>,
                     &k_bisect<PSB_KL, PSB_KU, false, 1, 2, false>,
                     &k_bisect<PSB_KL, PSB_KU, false, 1, 2, true>, &k_lanczos<PSB_KL, PSB_KU, false, D>,
-                    Ring<PSB_KL, PSB_KU, D>::BYTES, PSB_NP, PSB_G, BisRow<PSB_KL, PSB_KU>::BYTES};
+                    Ring<PSB_KL, PSB_KU, D>::BYTES + LUS<PSB_KL, PSB_KU>::BYTES, PSB_NP, PSB_G,
+                    BisRow<PSB_KL, PSB_KU>::BYTES};
 #endif
 
 struct Registrar {
