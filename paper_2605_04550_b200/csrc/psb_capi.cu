@@ -619,7 +619,14 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     Fit fw, fp;
     CK(fit(kp.bm, &fw));
     CK(fit(kp.bm2, &fp));
-    const bool pair = kp.bm2 != kp.bm && (h->k_bvariant == 2 || (h->k_bvariant == 0 && 2 * nB <= fp.threads));
+    // General bands (staged kernels, C5): engine L takes whole SMs first, so engine B runs mostly at full
+    // occupancy behind it, and a list of up to ~5 full-occupancy pair passes finishes sooner on the pair (its
+    // late points take half the latency): C5 matrices 1 / 63 (69 k / 60 k points) 301 -> 278, 391 -> 376 ms;
+    // matrices 0 / 17 (307 k / 228 k, 13 / 10 passes) lose on it (732 -> 782, 594 -> 632 ms) and keep the wide one.
+    const double pair_pass = (double)fp.occFull * h->num_sms * fp.tpb / 2.0;  // points per full pair pass
+    const bool short_general = bsw > 0 && (double)nB <= 5.0 * pair_pass;
+    const bool pair = kp.bm2 != kp.bm &&
+                      (h->k_bvariant == 2 || (h->k_bvariant == 0 && (2 * nB <= fp.threads || short_general)));
     // ((4,4) and the runtime shapes have one variant; PSB_BVARIANT=1/2 forces wide/pair for tests)
     if (pair) { kp.bm = kp.bm2; kp.np = 1; kp.g = 2; }
     const Fit& fc = pair ? fp : fw;
