@@ -131,3 +131,32 @@ def sharded_matrix_batch(matrices, grid, evaluate_field: Callable | None = None,
         from . import core
         evaluate_field = core.full_pseudospectrum
     return {i: evaluate_field(matrices[i], grid) for i in shard_indices(len(matrices), rank, world).tolist()}
+
+
+def gather_matrix_maps(maps: dict, count: int, shape, dst: int = 0, group=None, device=None):
+    """The batch's final gather (north star: "no NCCL except a final gather of the sigma_min map"): every
+    rank's maps from sharded_matrix_batch ({matrix index: (ny, nx) float64 values}) to rank `dst`, which
+    returns the full (count, ny, nx) stack; the other ranks return None. One collective of the largest
+    share per rank (ranks hold ceil(count/N) or floor(count/N) maps, padded with NaN to the same size).
+    Works with gloo (CPU tensors) and nccl (CUDA tensors, `device`)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    per = (count + world - 1) // world
+    ny, nx = shape
+    mine = shard_indices(count, rank, world)
+    buf = torch.full((per, ny, nx), float("nan"), dtype=torch.float64, device=device)
+    for k, i in enumerate(mine.tolist()):
+        v = maps[i]
+        v = v.values if hasattr(v, "values") else v
+        buf[k] = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(buf.device)
+    out = torch.empty((world * per, ny, nx), dtype=torch.float64, device=device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    if rank != dst:
+        return None
+    out = out.cpu().numpy().reshape(world, per, ny, nx)
+    full = np.empty((count, ny, nx))
+    for r in range(world):
+        idx = shard_indices(count, r, world)
+        full[idx] = out[r, : idx.size]
+    return full

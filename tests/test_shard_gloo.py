@@ -121,7 +121,9 @@ def _worker_batch(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     mats = [np.full((2, 2), float(i)) for i in range(7)]
     got = shard.sharded_matrix_batch(mats, None, evaluate_field=lambda A, g: float(A[0, 0]) * 10)
-    q.put((rank, got))
+    maps = {i: np.full((3, 4), v) + np.arange(12).reshape(3, 4) for i, v in got.items()}
+    full = shard.gather_matrix_maps(maps, len(mats), (3, 4))
+    q.put((rank, (got, full)))
     dist.destroy_process_group()
 
 
@@ -133,9 +135,14 @@ def test_gloo_world2_matrix_batch():
     procs = [ctx.Process(target=_worker_batch, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    out = dict(q.get(timeout=120) for _ in procs)
+    res = dict(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    out = {r: v[0] for r, v in res.items()}
     assert sorted(out[0]) == [0, 2, 4, 6] and sorted(out[1]) == [1, 3, 5]
     assert all(v == 10 * i for part in out.values() for i, v in part.items())
+    # the final gather: rank 0 holds every map in matrix order, the other rank nothing
+    assert res[1][1] is None
+    want = np.stack([np.full((3, 4), 10.0 * i) + np.arange(12).reshape(3, 4) for i in range(7)])
+    assert np.array_equal(res[0][1], want)
