@@ -73,6 +73,7 @@ struct psb_handle {
   double dr = 0.0, offsq = 0.0;
   double sscale = 1.0, zscale = 1.0;  // exact power-of-two problem scaling (psb_set_matrix)
   double anorm = 0.0;    // general-band kernels' split scale: sqrt(||A||_1 ||A||_inf) >= ||A||_2
+  double cert = INFINITY;  // engine L's singularity certificate base 1 / (delta max_j ||A e_j||)^2 (LanArgs)
   int tz_j0 = 1, tz_j1 = 0;  // interior rows sharing one G row (diagonal-constant band), empty by default
   // development knobs, read once at psb_create (A/B switches; defaults are the product path):
   //   PSB_TAU=x default engine split, PSB_BVARIANT=1/2 force the wide / pair bisection variant, PSB_NOBEXP=1 no second engine-B launch, PSB_BTPB=n engine-B block size, PSB_NOSEC=1 plain multisection, PSB_NOTZ=1 per-row G formation, PSB_LWARPS=N cap on
@@ -82,6 +83,7 @@ struct psb_handle {
   int k_refill = 16;
   int k_btpb = 128;
   double k_tau = 0.0;
+  double k_cert_delta = 1e-16;  // PSB_CERT_DELTA=x (0: certificates off, the round-2 overflow rule alone)
   bool k_bexpand = true, k_fallback = true, k_seq = false;
   int k_bvariant = 0;
   struct FitEntry { const void* f; int lkey, btpb, tpb, occ, occFull; int64_t threads; int wregs; };
@@ -195,6 +197,7 @@ int psb_create(int device, psb_handle** out) {
   h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 0;  // 0: pick per launch
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
   h->k_refill = getenv("PSB_REFILL") ? atoi(getenv("PSB_REFILL")) : 16;  // dev: engine-L refill threshold
+  h->k_cert_delta = getenv("PSB_CERT_DELTA") ? atof(getenv("PSB_CERT_DELTA")) : 1e-16;
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking) != cudaSuccess) { delete h; return PSB_ERR_CUDA; }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
@@ -286,6 +289,13 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
     for (int i = 0; i < n; i++) om[i] = std::min(off[i], offr[i]);
     CK(h->offmin.ensure(sizeof(double) * n));
     CK(cudaMemcpy(h->offmin.p, om.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    // Engine L's singularity certificates (LanArgs::tcert/ncert) prove sigma_min <= delta max_j ||A e_j||,
+    // and max_j ||A e_j|| <= ||A||_2: a point decided there is singular to working precision against the
+    // parity gate's floor 1e-14 ||A||_2. Computed on the scaled matrix the engines see.
+    double colmax2 = 0.0;
+    for (int i = 0; i < n; i++) colmax2 = std::max(colmax2, off[i] + std::norm(A[(int64_t)kl * n + i]));
+    const double dl = h->k_cert_delta;
+    h->cert = (dl > 0.0 && colmax2 > 0.0) ? 1.0 / (dl * dl * colmax2) : INFINITY;
     h->dc = make_double2(c.real(), c.imag());
     h->dr = r * (1.0 + 1e-15);
     h->offsq = *std::max_element(off.begin(), off.end()) * (1.0 + 1e-15);
@@ -554,6 +564,8 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     la.scratch = h->scratch.as<double2>(); la.pivs = h->pivs.as<int>();
     la.warp_stride = warp_stride; la.piv_stride = piv_stride;
     la.kmax = kmax; la.refill = std::min(32, std::max(1, opt.refill));
+    la.ncert = h->cert;
+    la.tcert = std::isfinite(h->cert) ? h->cert * (double)n * (1.0 + 2.0 * kl) : INFINITY;
     la.prof = nullptr;
     if (h->k_prof) {
       CK(h->prof.ensure(64));

@@ -79,6 +79,10 @@ struct LanArgs {
   int64_t warp_stride, piv_stride;
   int kmax, refill;
   unsigned long long* prof;       // optional: per-phase clock64 totals [lu, s1, s2, s3, s4, ritz, idle]
+  // Certificates of singularity to working precision (psb_set_matrix; INFINITY disables them): the point
+  // is decided as sigma = 0 (status 2) once sigma_min <= delta ||A e_j||_max <= delta ||A||_2 is proven,
+  // from the fused LU's prefix ||t[0..j]||^2 > tcert (t = U^{-H} v1) or from nu^2 = ||M^{-H} v1||^2 > ncert.
+  double tcert, ncert;
 };
 
 // ---------------------------------------------------------------- cp.async row ring
@@ -789,7 +793,7 @@ struct LUS {
 // decided by an exact zero pivot or a non-finite t_j (see the caller): both finish it as singular (status 2).
 template <int KL, int KU>
 __device__ bool lu_staged(int n, const double2* __restrict__ Ab, const double2* __restrict__ LUT, double2* stg,
-                          int lane, bool live, double2 z, LV FU, LV FL, LVb piv, LV Tn, LV Rn) {
+                          int lane, bool live, double2 z, LV FU, LV FL, LVb piv, LV Tn, LV Rn, double tcert) {
   constexpr int W = KL + KU, NU = W + 1, NL = (KL > 0 ? KL : 1);
   typedef LUS<KL, KU> SS;
   const unsigned FULL = 0xffffffffu;
@@ -813,6 +817,7 @@ __device__ bool lu_staged(int n, const double2* __restrict__ Ab, const double2* 
   double2 acc[W + 1];
 #pragma unroll
   for (int d = 0; d <= W; d++) acc[d] = czero();
+  double tt = 0.0;  // ||t[0..j]||^2
   auto fill = [&](int sidx, int j0) {
     double2* dst = stg + sidx * SS::SE;
 #pragma unroll
@@ -876,7 +881,11 @@ __device__ bool lu_staged(int n, const double2* __restrict__ Ab, const double2* 
 #pragma unroll
         for (int dd = 1; dd <= W; dd++) acc[dd - 1] = cfms_cj(acc[dd], u[dd - 1], tp);
         acc[W] = czero();
-        if (!(isfinite(t.x) && isfinite(t.y))) ok = false;
+        // t_j is final (forward solve), so ||t|| >= ||t[0..j]||; with M = P^T L U, |l| <= sqrt(2) (cabs1 pivots),
+        // ||L||_F^2 <= n (1 + 2 kl): sigma_min <= ||v1|| / ||M^{-H} v1|| <= ||L||_F / ||t[0..j]|| (||v1|| = 1),
+        // so tt > tcert = n (1 + 2 kl) / (delta ||A||)^2 proves sigma_min <= delta ||A|| (psb_set_matrix).
+        tt = fma(t.x, t.x, fma(t.y, t.y, tt));
+        if (!(isfinite(t.x) && isfinite(t.y)) || tt > tcert) ok = false;
       }
 #pragma unroll
       for (int r = 1; r <= KL; r++) {
@@ -998,7 +1007,7 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       const bool mine = phase == 1;
       const LV Tn = T, Rn = rsw ? RA0 : RB0;  // pl_s1 writes r into the current RB, then swaps
       const bool ok = lu_staged<(KL > 0 ? KL : 1), KU>(n, a.Ab, a.LUT, lstage, lane, mine, mine ? z : czero(),
-                                                       FU, FL, piv, Tn, Rn);
+                                                       FU, FL, piv, Tn, Rn, a.tcert);
       if (mine) {
         if (!ok) {
           finish(0.0, 0, 2);
@@ -1053,7 +1062,8 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       if (a.prof) { long long t = clock64(); if (lane == __ffs(__activemask()) - 1) atomicAdd(&a.prof[2], (unsigned long long)(t - tq1)); tq1 = t; }
       if (k == 1) {
         nu = sqrt(nrm);
-        if (!(nu > 0.0) || !isfinite(nu)) finish(0.0, 0, 2);  // singular to working precision
+        // singular to working precision: a non-finite nu, or nu^2 > ncert (sigma_min <= 1 / nu <= delta ||A||)
+        if (!(nu > 0.0) || !isfinite(nu) || nrm > a.ncert) finish(0.0, 0, 2);
       }
     }
     if (phase == 2) {

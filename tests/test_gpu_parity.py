@@ -346,3 +346,26 @@ def test_engine_b_variants_bitwise_equal(gpu, tmp_path, name):
                        cwd=str(Path(__file__).resolve().parents[1]))
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("name,count", [("C2", 24), ("C3", 8)])
+def test_singularity_certificate_points_are_below_the_floor(gpu, name, count):
+    """Engine L decides a point as singular to working precision (σ = 0, status 2) once it has proven
+    σ_min <= 1e-16 max_j ||A e_j|| (the LU prefix ||U^{-H} v1|| and nu = ||M^{-H} v1||
+    certificates). At every such point the reference's zgesdd must lie under the parity floor
+    1e-5 ||A||_2 * 1e-9 - in fact under 1e-15 ||A||_2 (its own rounding level), checked on a seeded sample
+    of the decided points of the full grid."""
+    from oracle.sigma_oracle import smin_restated
+    cfg = configs.CONFIGS[name]
+    A = cfg.matrix()
+    Ad = A.todense() if hasattr(A, "todense") else np.asarray(A)
+    zs = cfg.grid.points().ravel()
+    vals, iters, st = core.smin_many(A, zs, return_info=True)
+    dec = np.flatnonzero((st == 2) & (vals == 0.0))
+    assert dec.size > 0
+    pick = np.random.default_rng(5).choice(dec, min(count, dec.size), replace=False)
+    ref = smin_restated(Ad, zs[pick])
+    norm2 = np.linalg.norm(Ad, 2)
+    check(vals[pick], ref, norm2, f"{name} certified points")
+    assert ref.max() <= 1e-15 * norm2, f"{name}: certified point with reference sigma {ref.max():.3e}"
+    print(f"{name}: {dec.size} certified points; sample max reference sigma {ref.max() / norm2:.2e} ||A||_2")

@@ -44,7 +44,24 @@ for m in mats:
     a, b = np.load(f"/tmp/ab_a_{m}.npy"), np.load(f"/tmp/ab_b_{m}.npy")
     eq = np.array_equal(a, b)
     d = np.max(np.abs(a - b) / np.maximum(np.abs(a), 1e-300))
+    nd = int(np.sum(a != b))
+    dabs = float(np.max(np.abs(a - b))) / float(np.max(a))  # largest change against the map's scale
+    if nd:
+        sys.path.insert(0, '.')
+        from paper_2605_04550_b200 import configs
+        A = configs.CONFIGS[name].matrix(m)
+        if hasattr(A, "band"):  # band[d + kl, i] = A[i, i + d]: column i + d
+            c2 = np.zeros(A.n)
+            for d in range(-A.kl, A.ku + 1):
+                i = np.arange(max(0, -d), min(A.n, A.n - d))
+                c2[i + d] += np.abs(A.band[d + A.kl, i]) ** 2
+            cmax = float(np.sqrt(c2.max()))
+        else:
+            cmax = float(np.max(np.linalg.norm(np.asarray(A), axis=0)))
+        dm = a != b
+        print(f"  changed points: max |diff| / max_j ||A e_j|| = {np.max(np.abs(a - b)[dm]) / cmax:.2e}, "
+              f"A-side values there <= {np.max(a[dm]) / cmax:.2e} ||A e_j||, B-side <= {np.max(b[dm]) / cmax:.2e}")
     ta, tb = res["a"][str(m)], res["b"][str(m)]
-    print(f"{name} m={m}: bitwise {eq} (max rel {d:.2e}) | A total {ta['ms_total']:.1f} B {ta['ms_bisect']:.1f} "
+    print(f"{name} m={m}: bitwise {eq} (max rel {d:.2e}, {nd} differ, max|diff|/max {dabs:.1e}) | A total {ta['ms_total']:.1f} B {ta['ms_bisect']:.1f} "
           f"L {ta['ms_lanczos']:.1f} C {ta.get('ms_classify', 0):.1f} | B total {tb['ms_total']:.1f} "
           f"B {tb['ms_bisect']:.1f} L {tb['ms_lanczos']:.1f} C {tb.get('ms_classify', 0):.1f} ms")
