@@ -3,10 +3,12 @@
 
 Headline workload (BASELINE.json configs[4], the config the 1/2/4/8-GPU metric is
 quoted on): 64 seeded noisy banded Toeplitz matrices, n=4000, (kl,ku)=(3,3), complex128, a full
-1024 x 1024 grid each. One step = one whole matrix per GPU: rank r evaluates matrix
-(s*N + r) mod 64 at step s, so the steps walk through distinct matrices of the batch. The matrices
-are independent objects, dealt over the ranks with no data-path collective: per-GPU
-work is fixed as N grows ("scaling": "weak"). Each rank keeps the σ maps it computed.
+1024 x 1024 grid each. One step = one pass over the whole batch (64 x 1,048,576 σ_min) by all GPUs
+together ("scaling": "strong"): the ranks pull whole matrices from one counter in the process group's
+store, in longest-first order of a subgrid cost estimate (shard.dynamic_matrix_batch; the matrices'
+costs differ 250x, so a fixed deal would leave most GPUs idle behind the slowest). The matrices are
+independent objects: no data-path collective; each rank keeps the σ maps it computed. A
+pass takes as long as its busiest rank's device time (max over ranks per pass).
 
 --config C1..C4 are the single-matrix configs (secondary lines). Their fixed grid is dealt cyclically
 (point p -> rank p mod N, shard.py) and the σ map is all-gathered over NCCL inside every step, the
@@ -51,7 +53,7 @@ METRIC = "sigma_min(zI-A) grid points/sec at 1/2/4/8 B200; % of per-z FP64/HBM r
 UNIT = "points/s"
 WORKLOAD = {
     "C5": "C5: 64 seeded noisy banded Toeplitz n=4000 (3,3) complex128, full 1024x1024 grid per matrix; "
-          "one step = one whole matrix per GPU, matrix (step*N + rank) mod 64",
+          "one step = one pass over the whole batch (64 x 1,048,576 sigma_min) on all GPUs together",
     "C4": "C4: convection-diffusion n=2000 Pe=50 (1,1), fixed 512x512 grid dealt over the GPUs",
     "C3": "C3: complex banded Toeplitz n=1000 (2,3), fixed 256x256 grid dealt over the GPUs",
     "C2": "C2: Grcar n=400 (1,3), fixed 200x200 grid over [-1,3]x[-3.5,3.5] dealt over the GPUs",
@@ -66,6 +68,8 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5", help="workload C1..C5; C5 (BASELINE configs[4]) is the headline")
+    ap.add_argument("--matrices", type=int, default=0,
+                    help="C5 development runs: the first M matrices of the batch (default: all 64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-guided", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help=argparse.SUPPRESS)
@@ -245,7 +249,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-        "higher_is_better": True, "scaling": "weak" if args.config == "C5" else "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (seeded BASELINE config)",
         "config": {"workload": WORKLOAD[args.config], "sample_points_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": how, **host_info()},
@@ -367,15 +371,18 @@ def run_ours(args, rank, world, local_rank):
     grid = cfg.grid
     batch = cfg.batch > 1
     pts = grid.points().ravel()
-    if batch:  # whole matrices per rank: every rank evaluates the full grid of its own matrix
+    if batch:
+        # One step = one pass over the batch, all ranks together: ranks pull whole matrices (every rank
+        # evaluates the full grid of the matrices it pulls) from the process group's store counter in
+        # longest-first order of a subgrid cost estimate (shard.py). No data-path collective.
+        nmat = min(args.matrices, cfg.batch) if args.matrices > 0 else cfg.batch
         mine = pts
-        mats = {}
-
-        def matrix_of(step):
-            m = (step * world + rank) % cfg.batch
-            if m not in mats:
-                mats[m] = cfg.matrix(m)
-            return m, mats[m]
+        mats = [cfg.matrix(m) for m in range(nmat)]
+        t_plan = time.perf_counter()
+        costs = shard.batch_cost_estimates(mats, grid, device=local_rank)
+        order = shard.lpt_order(costs)
+        plan_s = time.perf_counter() - t_plan
+        store = shard.default_store()
     else:
         mine = np.ascontiguousarray(pts[rank::world])
         A0 = cfg.matrix(0)
@@ -395,13 +402,6 @@ def run_ours(args, rank, world, local_rank):
     # to its own unordered stream): the L2 flush, the step's kernels and the timing events are then ordered
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    used = []
-
-    def prepare(step):  # outside the timed region: the step's matrix resident on the device
-        m, A = matrix_of(step)
-        with h.lock:
-            core._set_matrix(h, A)
-        used.append(m)
 
     def step():
         rc = h.lib.psb_smin_points_device(h.h, C.c_void_p(d_zs.data_ptr()), P, None,
@@ -417,65 +417,102 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
-    sampler = ClockSampler(local_rank)  # covers warm-up, the timed steps and the e2e leg
-    sampler.start()
-    time.sleep(0.3)
-    s_idx = 0
-    for _ in range(max(args.warmup, 0)):
-        prepare(s_idx)
-        step()
-        s_idx += 1
-    torch.cuda.synchronize()
-    st = d_status.cpu().numpy()
-    assert (st <= 2).all(), "non-converged points in the benchmark step"
-
-    stats, step_ms = [], []
-    barrier()
-    torch.cuda.synchronize()
-    for _ in range(args.steps):
-        prepare(s_idx)
-        s_idx += 1
-        flush.random_(0, 255)  # evict L2 (256 MiB > 126 MB) between timed steps, outside the events
-        barrier()
+    def timed_item(A):
+        """One matrix's sweep: the band resident on the device and L2 flushed first (outside the events)."""
+        with h.lock:
+            core._set_matrix(h, A)
+        flush.random_(0, 255)  # evict L2 (256 MiB > 126 MB) between timed sweeps, outside the events
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         step()
         e1.record(stream)
         e1.synchronize()
-        step_ms.append(e0.elapsed_time(e1))
-        stats.append(h.stats())
-        assert (d_status.cpu().numpy() <= 2).all(), "non-converged points in a timed step"
-    torch.cuda.synchronize()
-    barrier()
+        st_ = h.stats()
+        assert (d_status.cpu().numpy() <= 2).all(), "non-converged points in a timed sweep"
+        return e0.elapsed_time(e1), st_
 
-    # max over ranks of the summed step time (each rank runs the same number of steps)
-    t = torch.tensor([float(np.sum(step_ms))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item()) / args.steps
-    units = world * P if batch else pts.size  # points every rank together finishes per step
+    sampler = ClockSampler(local_rank)  # covers warm-up, the timed steps and the e2e leg
+    sampler.start()
+    time.sleep(0.3)
+    stats, step_ms, pass_items = [], [], []
+    if batch:
+        def run_pass(key):
+            """This rank's share of one pass: [(matrix, device ms, stats)] of the matrices it pulled."""
+            return [(m, *timed_item(mats[m])) for m in shard.dynamic_items(order, key, store)]
+
+        for w in range(max(args.warmup, 0)):
+            run_pass(f"bench/warmup{w}")
+            barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            items = run_pass(f"bench/step{k}")
+            barrier()
+            pass_items.append(items)
+            step_ms.append(float(sum(ms_ for _, ms_, _ in items)))  # this rank's device time in the pass
+            stats.extend(st_ for _, _, st_ in items)
+        torch.cuda.synchronize()
+        # the step (pass) takes as long as its busiest rank: max over ranks per pass
+        tp = torch.tensor(step_ms, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+        ms = float(tp.mean().item())
+        units = nmat * P  # points every rank together finishes per step
+    else:
+        with h.lock:
+            core._set_matrix(h, matrix_of(0)[1])
+        for _ in range(max(args.warmup, 0)):
+            step()
+        torch.cuda.synchronize()
+        assert (d_status.cpu().numpy() <= 2).all(), "non-converged points in the benchmark step"
+        barrier()
+        torch.cuda.synchronize()
+        A0m = matrix_of(0)[1]
+        for _ in range(args.steps):
+            ms_, st_ = timed_item(A0m)
+            barrier()
+            step_ms.append(ms_)
+            stats.append(st_)
+        torch.cuda.synchronize()
+        barrier()
+        # max over ranks of the summed step time (each rank runs the same number of steps)
+        t = torch.tensor([float(np.sum(step_ms))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item()) / args.steps
+        units = pts.size
     value = units / (ms * 1e-3)
 
     # ---- e2e through the public API, host buffers, copies inside the timed region
     e2e_ms, h2d, d2h = [], 0, 0
-    if not args.no_e2e:
-        for it in range(args.warmup + min(args.steps, 3 if batch else args.steps)):
-            m, A = matrix_of(s_idx)
-            s_idx += 1
+    if not args.no_e2e and batch:
+        # one pass over the batch through the public API (host band and axes in, the σ map and status out, per
+        # matrix), the same queue and order; the pass ends when the last rank finishes (max over ranks)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for m in shard.dynamic_items(order, "bench/e2e", store):
+            core.full_pseudospectrum(mats[m], grid, device=local_rank)
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        h2d = sum(A.band.size * 16 + (grid.nx + grid.ny) * 8 for A in mats)  # the whole batch, every rank's share
+        d2h = nmat * grid.size * 9  # σ (f64) + status (i8) of every map
+    elif not args.no_e2e:
+        A = matrix_of(0)[1]
+        for it in range(args.warmup + args.steps):
             barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            if batch or world == 1:
-                fld = core.full_pseudospectrum(A, grid, device=local_rank)
+            if world == 1:
+                core.full_pseudospectrum(A, grid, device=local_rank)
             else:
-                fld = shard.sharded_full_pseudospectrum(A, grid)
+                shard.sharded_full_pseudospectrum(A, grid)
             torch.cuda.synchronize()
             dt = (time.perf_counter() - t0) * 1e3
             if it >= args.warmup:
                 e2e_ms.append(dt)
-            band_bytes = A.band.size * 16
-        if batch or world == 1:
+        band_bytes = A.band.size * 16
+        if world == 1:
             h2d = band_bytes + (grid.nx + grid.ny) * 8
             d2h = grid.size * 9  # σ (f64) + status (i8)
         else:
@@ -547,15 +584,21 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak" if batch else "strong", "vs_baseline": None, "dtype": "c128",
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded BASELINE config, no dataset)",
-            "config": {"workload": WORKLOAD[name], "grid": f"{grid.ny}x{grid.nx}", "points_per_gpu": P,
+            "config": {"workload": WORKLOAD[name], "grid": f"{grid.ny}x{grid.nx}",
+                       "points_per_gpu": units / world if batch else P,
                        "points_per_step": units,
-                       "matrices_timed_rank0": used[args.warmup:args.warmup + args.steps] if batch else [0],
-                       "sharding": ("matrices dealt over ranks (matrix (step*N + rank) mod 64), no collective"
+                       **({"matrices": nmat,
+                           "matrices_rank0_per_pass": [len(it) for it in pass_items],
+                           "schedule": "ranks pull whole matrices from one store counter in longest-first order "
+                                       "of a cost estimate (engine split on every 16th grid point each way); "
+                                       "no data-path collective; a pass takes its busiest rank's device time",
+                           "plan_s": plan_s} if batch else {}),
+                       "sharding": ("whole matrices per rank, LPT dynamic queue (shard.dynamic_matrix_batch)"
                                     if batch else "cyclic point p -> rank p mod N; sigma map all-gathered over "
                                                   "NCCL inside every step"),
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "l2": "flushed before every timed matrix sweep (256 MiB write, outside the events)",
                        "parallelism": f"dp{world}"},
             "roofline": roof,
             "roofline_kernels": kerns,
@@ -563,10 +606,13 @@ def run_ours(args, rank, world, local_rank):
                                     "points_per_s": roof_pts * world if roof_pts else None,
                                     "frac": value / (roof_pts * world) if roof_pts else None},
             "lu_solve_model": model,
-            "phases_ms": [{"matrix": (used[args.warmup + i] if batch else 0), "step": round(step_ms[i], 3),
-                           **{k[3:]: round(st_[k], 3) for k in ("ms_total", "ms_classify", "ms_bisect", "ms_lanczos",
-                                                              "ms_fallback")}}
-                          for i, st_ in enumerate(stats)],
+            "phases_ms": ([{"matrix": m, "sweep": round(ms_, 3),
+                            **{k[3:]: round(st_[k], 3) for k in ("ms_classify", "ms_bisect", "ms_lanczos", "ms_fallback")}}
+                           for m, ms_, st_ in pass_items[0]] if batch else
+                          [{"step": round(step_ms[i], 3),
+                            **{k[3:]: round(st_[k], 3) for k in ("ms_total", "ms_classify", "ms_bisect", "ms_lanczos",
+                                                               "ms_fallback")}}
+                           for i, st_ in enumerate(stats)]),
             "engines": {"lanczos_points": S["n_lanczos"] // K, "bisect_points": S["n_bisect"] // K,
                         "lanczos_steps": S["lanczos_iters"] // K, "pd_tests": S["pd_tests"] // K},
             "gpu_launches": int(S["launches"]),
@@ -574,7 +620,8 @@ def run_ours(args, rank, world, local_rank):
         }
         if e2e_value is not None:
             line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                           "api": ("core.full_pseudospectrum (one matrix per rank)" if batch or world == 1
+                           "api": ("core.full_pseudospectrum per matrix, matrices from the LPT queue (one pass)"
+                                   if batch else "core.full_pseudospectrum" if world == 1
                                    else "shard.sharded_full_pseudospectrum")}
         if cpu:
             line["cpu_baseline"] = cpu

@@ -13,6 +13,7 @@
  *   psb_smin_grid         <- pseudospec/core.py:177-195 full_pseudospectrum (region == NULL) and
  *                            pseudospec/core.py:198-208 restricted_field (region != NULL)
  *   psb_smin_points_device   same as psb_smin_points on device-resident buffers (no host copies)
+ *   psb_engine_split      the engine split's counts on a point set (batch scheduling estimate)
  *   psb_predict_points    <- pseudospec/pipeline.py:169-172 _predict_points (+ features.py:129-164,
  *                            network.py:62-92,153-190)
  *   psb_region_select     <- pseudospec/pipeline.py:227-231 predicted_region (+ core.py:224-231 dilate)
@@ -106,6 +107,12 @@ int psb_smin_grid(psb_handle* h, const double* xs, int32_t nx, const double* ys,
  * may be NULL); stream is a cudaStream_t (NULL = library stream). Synchronous. */
 int psb_smin_points_device(psb_handle* h, const double* d_zs, int64_t P, const psb_opts* opts,
                            double* d_sigma, int32_t* d_iters, int8_t* d_status, void* stream);
+
+/* Engine split of a point set, without sigma: the classification test alone (one LDL^H test per point,
+ * the same test psb_smin_points starts with), returning how many points the bisection and Lanczos
+ * engines would take. Batch scheduling uses it on a coarse subgrid as a matrix's cost estimate (no
+ * reference counterpart: the reference's process pool deals fixed row blocks, core.py:186-195). */
+int psb_engine_split(psb_handle* h, const double* zs, int64_t P, int64_t* n_bisect, int64_t* n_lanczos);
 
 int psb_get_stats(const psb_handle* h, psb_stats* out);
 

@@ -24,7 +24,7 @@ PSB_OK, PSB_ERR_PARAM, PSB_ERR_NUMERICAL, PSB_ERR_CUDA, PSB_ERR_IO = 0, 1, 2, 3,
 #: every symbol include/psb200.h declares (checked by the CPU test-suite)
 EXPORTS = (
     "psb_create", "psb_destroy", "psb_last_error", "psb_version", "psb_set_matrix",
-    "psb_smin_points", "psb_smin_grid", "psb_smin_points_device", "psb_get_stats",
+    "psb_smin_points", "psb_smin_grid", "psb_smin_points_device", "psb_engine_split", "psb_get_stats",
     "psb_predict_points", "psb_region_select", "psb_smin_selection", "psb_fp64_peak", "psb_recall_sweep",
     "psb_write_field_csv", "psb_write_mask_csv",
 )
@@ -83,6 +83,7 @@ def load_library(path: Path | str | None = None) -> C.CDLL:
         lib.psb_smin_grid.argtypes = [_P, _P, C.c_int32, _P, C.c_int32, _P, C.POINTER(Opts), _P, _P,
                                       _P, C.POINTER(C.c_int64)]
         lib.psb_smin_points_device.argtypes = [_P, _P, C.c_int64, C.POINTER(Opts), _P, _P, _P, _P]
+        lib.psb_engine_split.argtypes = [_P, _P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         lib.psb_get_stats.argtypes = [_P, C.POINTER(Stats)]
         lib.psb_fp64_peak.argtypes = [_P, C.POINTER(C.c_double)]
         lib.psb_recall_sweep.argtypes = [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, _P]

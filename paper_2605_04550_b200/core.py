@@ -273,6 +273,23 @@ def smin_many(A, zs: np.ndarray, label: str = "matrix", chunk: int = 512, *,
     return out
 
 
+def engine_split(A, zs: np.ndarray, *, device: int | None = None) -> tuple[int, int]:
+    """How many of the shifts `zs` the bisection and the Lanczos engine would take (the classification
+    test alone, no σ): the cost estimate batch scheduling uses (shard.batch_cost_estimates)."""
+    zs = np.ascontiguousarray(np.asarray(zs, dtype=complex).ravel())
+    band = as_band(A)
+    h = _lib.handle(device)
+    nb, nl = C.c_int64(0), C.c_int64(0)
+    with h.lock:
+        _set_matrix(h, band)
+        rc = h.lib.psb_engine_split(h.h, zs.ctypes.data_as(C.c_void_p), zs.size, C.byref(nb), C.byref(nl))
+        if rc == _lib.PSB_ERR_PARAM:
+            raise ParameterError(h.error())
+        if rc != _lib.PSB_OK:
+            raise RuntimeError(f"psb_engine_split failed ({rc}): {h.error()}")
+    return int(nb.value), int(nl.value)
+
+
 def smin_at(A, z: complex, label: str = "matrix", *, device: int | None = None) -> float:
     """σ_min of z I - A at one point (core.py:131-138); identical bits to smin_many."""
     z = complex(z)

@@ -168,6 +168,7 @@ static bool pick(int kl, int ku, KPair* out) {
 }
 
 static bool fallback_off(const psb_handle* h);
+static constexpr int kClassifyOnly = 3;  // internal force_engine value of psb_engine_split
 static int default_kmax(int n) { return std::min(3000, std::max(64, 4 * n)); }
 
 extern "C" {
@@ -431,7 +432,8 @@ static double bytes_it_row(int kl, int ku) {
 
 // Core pipeline on device buffers. zs/outidx/out/iters/status are device pointers.
 static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_outidx, int64_t P, double* d_out,
-                        int32_t* d_iters, int8_t* d_status, const psb_opts* o, cudaStream_t st) {
+                        int32_t* d_iters, int8_t* d_status, const psb_opts* o, cudaStream_t st,
+                        int force_override = -1) {
   psb_opts opt{};
   // Engine split: 1.5e-3 below n = 1000, 1e-3 from there (model error <= 7e-11 / 1.7e-10).
   // A function of the matrix only, so every sigma stays a function of (A, z). Measured per config:
@@ -442,9 +444,10 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     if (o->tau > 0) opt.tau = o->tau;
     if (o->bis_rtol > 0) opt.bis_rtol = o->bis_rtol;
     if (o->kmax > 0) opt.kmax = o->kmax;
-    opt.force_engine = o->force_engine;
+    opt.force_engine = (o->force_engine >= 0 && o->force_engine <= 2) ? o->force_engine : 0;
     if (o->refill > 0) opt.refill = o->refill;
   }
+  if (force_override >= 0) opt.force_engine = force_override;  // internal modes (kClassifyOnly)
   const int n = h->n, kl = h->kl, ku = h->ku;
   const int kmax = opt.kmax > 0 ? opt.kmax : default_kmax(n);
   KPair kp;
@@ -455,7 +458,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   h->stats.n_points = P;
   if (P == 0) return PSB_OK;
 
-  CK(h->counters.ensure(sizeof(unsigned long long) * 24));  // [16..19]: row counters (classify, B, fallback, B2)
+  CK(h->counters.ensure(sizeof(unsigned long long) * 24));  // [16..19]: row counters (classify, B, fallback, B2), [20] LU rows
   CK(h->listA.ensure(sizeof(int64_t) * P));
   CK(h->listB.ensure(sizeof(int64_t) * P));
   CK(h->listF.ensure(sizeof(int64_t) * P));
@@ -517,6 +520,14 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   CK(cudaMemcpyAsync(hc0, cnt, sizeof(hc0), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const int64_t nA = (int64_t)hc0[1], nB = (int64_t)hc0[7];
+  if (opt.force_engine == kClassifyOnly) {  // psb_engine_split: the split's counts, no sigma
+    h->stats.n_bisect = nB; h->stats.n_lanczos = nA;
+    float msC0 = 0.f;
+    cudaEventElapsedTime(&msC0, h->ev[0], h->ev[1]);
+    h->stats.ms_classify = msC0; h->stats.ms_total = msC0;
+    h->stats.launches = 1;
+    return PSB_OK;
+  }
   CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));  // reset the work counter
 
   // ---- engine L (band LU + inverse Lanczos) on stream2, concurrently with engine B
@@ -783,8 +794,9 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     S.flops_bisect = (r1 + r2) * ldl + (tzk ? pts_b * nb1 * flops_g_row(kl, ku)
                                             : (r1 / np1 + r2 / np2) * flops_g_row_aha(kl, ku));
   }
-  S.flops_lanczos = (double)hc[6] * n * flops_lu_row(kl, ku) + (double)hc[5] * n * flops_it_row(kl, ku);
-  S.bytes_lanczos = (double)hc[6] * n * (16.0 * (s.NU + kl) + 4.0) + (double)hc[5] * n * bytes_it_row(kl, ku);
+  // LU rows as counted by engine L (a decided point's factorization stops early), sweeps n rows per step
+  S.flops_lanczos = (double)hc[20] * flops_lu_row(kl, ku) + (double)hc[5] * n * flops_it_row(kl, ku);
+  S.bytes_lanczos = (double)hc[20] * (16.0 * (s.NU + kl) + 4.0) + (double)hc[5] * n * bytes_it_row(kl, ku);
   S.ms_bisect = msB; S.ms_lanczos = msL; S.ms_total = msT; S.ms_classify = msC; S.ms_fallback = msF;
   S.launches = 1 + (gridL > 0 ? 1 : 0) + (nB > 0 ? 1 : 0) + (gridB2 > 0 ? 1 : 0) + (ran_fallback ? 1 : 0);
   S.grid_bisect = (int32_t)(gridB + gridB2); S.grid_lanczos = (int32_t)gridL;
@@ -858,6 +870,30 @@ int psb_smin_points(psb_handle* h, const double* zs, int64_t P, const psb_opts* 
   if (status) std::memcpy(status, h->pin.at<char>(ot), (size_t)P);
   const int8_t* stat_h = h->pin.at<int8_t>(ot);
   return check_status(h, stat_h, nullptr, P, fail_index);
+}
+
+int psb_engine_split(psb_handle* h, const double* zs, int64_t P, int64_t* n_bisect, int64_t* n_lanczos) {
+  if (!h) return PSB_ERR_PARAM;
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (!h->have_matrix) return fail(h, PSB_ERR_PARAM, "no matrix set");
+  if (P < 0 || (P > 0 && !zs) || !n_bisect || !n_lanczos) return fail(h, PSB_ERR_PARAM, "bad point arguments");
+  for (int64_t i = 0; i < 2 * P; i++)
+    if (!std::isfinite(zs[i])) return fail(h, PSB_ERR_PARAM, "non-finite shift point");
+  *n_bisect = 0; *n_lanczos = 0;
+  if (P == 0) { h->stats = psb_stats{}; return PSB_OK; }
+  DeviceGuard dg(h->device);
+  cudaStream_t st = h->stream;
+  CK(h->zs.ensure(sizeof(double2) * P));
+  CK(h->out.ensure(sizeof(double) * P));
+  CK(h->iters.ensure(sizeof(int32_t) * P));
+  CK(h->status.ensure(sizeof(int8_t) * P));
+  CK(cudaMemcpyAsync(h->zs.p, zs, sizeof(double2) * P, cudaMemcpyHostToDevice, st));
+  const int rc = run_pipeline(h, h->zs.as<double2>(), nullptr, P, h->out.as<double>(), h->iters.as<int32_t>(),
+                              h->status.as<int8_t>(), nullptr, st, kClassifyOnly);
+  if (rc != PSB_OK) return rc;
+  *n_bisect = h->stats.n_bisect;
+  *n_lanczos = h->stats.n_lanczos;
+  return PSB_OK;
 }
 
 }  // extern "C"

@@ -68,7 +68,8 @@ struct LanArgs {
   const double2* __restrict__ zs;
   const int64_t* __restrict__ outidx;
   const int64_t* __restrict__ listA;
-  unsigned long long* counters;   // [1] nA (read), [4] work, [5] lanczos steps, [6] nL, [8] n not converged
+  unsigned long long* counters;   // [1] nA (read), [4] work, [5] lanczos steps, [6] nL, [8] n not converged,
+                                  // [20] LU rows factored (roofline accounting: the LU of a decided point stops early)
   double zscale, sscale;          // exact power-of-two scaling (see BisArgs)
   int64_t* listF;                 // not-converged points (as ~p: forced bisection entries), counters[8] of them
   double* out;
@@ -793,7 +794,8 @@ struct LUS {
 // decided by an exact zero pivot or a non-finite t_j (see the caller): both finish it as singular (status 2).
 template <int KL, int KU>
 __device__ bool lu_staged(int n, const double2* __restrict__ Ab, const double2* __restrict__ LUT, double2* stg,
-                          int lane, bool live, double2 z, LV FU, LV FL, LVb piv, LV Tn, LV Rn, double tcert) {
+                          int lane, bool live, double2 z, LV FU, LV FL, LVb piv, LV Tn, LV Rn, double tcert,
+                          int* rows_done) {
   constexpr int W = KL + KU, NU = W + 1, NL = (KL > 0 ? KL : 1);
   typedef LUS<KL, KU> SS;
   const unsigned FULL = 0xffffffffu;
@@ -818,6 +820,7 @@ __device__ bool lu_staged(int n, const double2* __restrict__ Ab, const double2* 
 #pragma unroll
   for (int d = 0; d <= W; d++) acc[d] = czero();
   double tt = 0.0;  // ||t[0..j]||^2
+  int nrows = 0;    // rows this lane's point factored
   auto fill = [&](int sidx, int j0) {
     double2* dst = stg + sidx * SS::SE;
 #pragma unroll
@@ -857,7 +860,7 @@ __device__ bool lu_staged(int n, const double2* __restrict__ Ab, const double2* 
           for (int c = 0; c <= W; c++) { const double2 t = win[0][c]; win[0][c] = win[r][c]; win[r][c] = t; }
         }
       }
-      if (ok) piv.put(j, p);
+      if (ok) { piv.put(j, p); nrows++; }
       const double2 d = win[0][0];
       double2 ri;
       if (d.x == 0.0 && d.y == 0.0) { ok = false; ri = czero(); }
@@ -917,6 +920,7 @@ __device__ bool lu_staged(int n, const double2* __restrict__ Ab, const double2* 
   }
   cp_wait<0>();
   __syncwarp();
+  *rows_done = nrows;
   return ok;
 }
 
@@ -1006,8 +1010,12 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       // overflows a few hundred rows in, C5).
       const bool mine = phase == 1;
       const LV Tn = T, Rn = rsw ? RA0 : RB0;  // pl_s1 writes r into the current RB, then swaps
+      int lrows = 0;
       const bool ok = lu_staged<(KL > 0 ? KL : 1), KU>(n, a.Ab, a.LUT, lstage, lane, mine, mine ? z : czero(),
-                                                       FU, FL, piv, Tn, Rn, a.tcert);
+                                                       FU, FL, piv, Tn, Rn, a.tcert, &lrows);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) lrows += __shfl_xor_sync(FULL, lrows, off);
+      if (lane == 0) atomicAdd(&a.counters[20], (unsigned long long)lrows);
       if (mine) {
         if (!ok) {
           finish(0.0, 0, 2);

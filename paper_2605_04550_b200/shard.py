@@ -133,30 +133,124 @@ def sharded_matrix_batch(matrices, grid, evaluate_field: Callable | None = None,
     return {i: evaluate_field(matrices[i], grid) for i in shard_indices(len(matrices), rank, world).tolist()}
 
 
+# ------------------------------------------------------------------ matrix batches: LPT dynamic queue
+# C5's matrices differ in cost by 250x (4 ms .. 1.05 s per 1024^2 map on one B200, tools/c5_balance.py): the
+# share of grid points outside the pseudospectrum (bisection engine) sets a matrix's cost. Dealing whole
+# matrices cyclically makes the slowest rank's sum the job time (modelled efficiency 0.65 / 0.47 / 0.37 at
+# N = 2 / 4 / 8 over the 64 measured maps), and splitting every matrix over the ranks multiplies each
+# launch's latency-bound tail (0.84 / 0.65 / 0.48). So ranks pull whole matrices from one shared counter in
+# longest-first (LPT) order of a cheap cost estimate: modelled 1.00 / 0.998 / 0.982 with the estimate below
+# (tools/c5_costmodel.py). The counter lives in the process group's store (host side); the data path has no
+# collective.
+SPLIT_STRIDE = 16  # cost-estimate subgrid: every 16th grid point each way (4,096 points of a 1024^2 grid)
+# Cost model fitted by tools/c5_costmodel.py over the 64 C5 maps (rank correlation 0.98 with the measured
+# device time): ms ~ 0.407 (subgrid bisection points) + 0.0111 (subgrid Lanczos points); only the ratio
+# matters for the order.
+BIS_WEIGHT, LAN_WEIGHT = 1.0, 0.0273
+
+
+def batch_cost_estimates(matrices, grid, stride: int = SPLIT_STRIDE, device=None) -> np.ndarray:
+    """Per-matrix cost estimate: the engine split (core.engine_split, one classification test per point) on
+    a coarse subgrid. Deterministic, so every rank computes the same estimates and order without exchange."""
+    from . import core
+    sub = np.ascontiguousarray(grid.points()[::stride, ::stride].ravel())
+    est = np.empty(len(matrices))
+    for i, A in enumerate(matrices):
+        nb, nl = core.engine_split(A, sub, device=device)
+        est[i] = BIS_WEIGHT * nb + LAN_WEIGHT * nl
+    return est
+
+
+def lpt_order(costs) -> list[int]:
+    """Longest-processing-time-first order (ties by index)."""
+    return sorted(range(len(costs)), key=lambda i: (-float(costs[i]), i))
+
+
+class LocalCounter:
+    """Single-process stand-in for the store's atomic counter."""
+
+    def __init__(self):
+        self._v = {}
+
+    def add(self, key, amount):
+        self._v[key] = self._v.get(key, 0) + amount
+        return self._v[key]
+
+
+def default_store():
+    """The process group's key-value store (TCPStore under torchrun), or a local counter without one."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        from torch.distributed import distributed_c10d
+        return distributed_c10d._get_default_store()
+    return LocalCounter()
+
+
+def dynamic_items(order, key: str, store=None):
+    """Yield the items of `order` this rank pulls from the shared counter `key` (each item goes to exactly
+    one rank: the store's add is atomic). Every pass over a batch needs a fresh key."""
+    store = default_store() if store is None else store
+    while True:
+        k = int(store.add(key, 1)) - 1
+        if k >= len(order):
+            return
+        yield order[k]
+
+
+def dynamic_matrix_batch(matrices, grid, evaluate_field: Callable | None = None, order=None, key: str = "psb/batch",
+                         store=None, device=None) -> dict:
+    """σ maps of a batch of matrices on one grid (BASELINE C5), matrices pulled by the ranks from a shared
+    LPT-ordered queue. Returns {matrix index: SigmaField} for the matrices this rank computed; the maps stay
+    on their rank (gather_matrix_maps collects them). `order` defaults to lpt_order(batch_cost_estimates(...))."""
+    if evaluate_field is None:
+        from . import core
+
+        def evaluate_field(A, g):
+            return core.full_pseudospectrum(A, g, device=device)
+    if order is None:
+        order = lpt_order(batch_cost_estimates(matrices, grid, device=device))
+    return {i: evaluate_field(matrices[i], grid) for i in dynamic_items(order, key, store)}
+
+
 def gather_matrix_maps(maps: dict, count: int, shape, dst: int = 0, group=None, device=None):
     """The batch's final gather (north star: "no NCCL except a final gather of the sigma_min map"): every
-    rank's maps from sharded_matrix_batch ({matrix index: (ny, nx) float64 values}) to rank `dst`, which
-    returns the full (count, ny, nx) stack; the other ranks return None. One collective of the largest
-    share per rank (ranks hold ceil(count/N) or floor(count/N) maps, padded with NaN to the same size).
-    Works with gloo (CPU tensors) and nccl (CUDA tensors, `device`)."""
+    rank's maps ({matrix index: (ny, nx) float64 values or SigmaField}, from sharded_matrix_batch or
+    dynamic_matrix_batch - any ownership) to rank `dst`, which returns the full (count, ny, nx) stack; the
+    other ranks return None. Two collectives: the per-rank map counts, then one all-gather of every rank's
+    maps padded with NaN to the largest share, each with its matrix indices (-1 = padding). Works with gloo
+    (CPU tensors) and nccl (CUDA tensors, `device`)."""
     import torch
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    per = (count + world - 1) // world
     ny, nx = shape
-    mine = shard_indices(count, rank, world)
+    mine = sorted(maps)
+    cnt = torch.tensor([len(mine)], dtype=torch.int64, device=device)
+    cnts = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(cnts, cnt, group=group)
+    per = max(1, int(cnts.max().item()))
     buf = torch.full((per, ny, nx), float("nan"), dtype=torch.float64, device=device)
-    for k, i in enumerate(mine.tolist()):
+    idx = torch.full((per,), -1, dtype=torch.int64, device=device)
+    for k, i in enumerate(mine):
         v = maps[i]
         v = v.values if hasattr(v, "values") else v
         buf[k] = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(buf.device)
+        idx[k] = int(i)
     out = torch.empty((world * per, ny, nx), dtype=torch.float64, device=device)
+    oidx = torch.empty(world * per, dtype=torch.int64, device=device)
     dist.all_gather_into_tensor(out, buf, group=group)
+    dist.all_gather_into_tensor(oidx, idx, group=group)
     if rank != dst:
         return None
-    out = out.cpu().numpy().reshape(world, per, ny, nx)
-    full = np.empty((count, ny, nx))
-    for r in range(world):
-        idx = shard_indices(count, r, world)
-        full[idx] = out[r, : idx.size]
+    out = out.cpu().numpy()
+    oidx = oidx.cpu().numpy()
+    full = np.full((count, ny, nx), np.nan)
+    seen = np.zeros(count, dtype=bool)
+    for k, i in enumerate(oidx.tolist()):
+        if i >= 0:
+            if seen[i]:
+                raise ValueError(f"matrix {i} held by more than one rank")
+            full[i] = out[k]
+            seen[i] = True
+    if not seen.all():
+        raise ValueError(f"matrices missing from the gather: {np.flatnonzero(~seen).tolist()}")
     return full

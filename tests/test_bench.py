@@ -48,3 +48,19 @@ def test_bench_line_on_gpu():
     assert line["gpu_launches"] >= 3 * 2
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert line["engines"]["lanczos_points"] + line["engines"]["bisect_points"] == 2500
+
+
+@pytest.mark.gpu
+def test_bench_c5_batch_pass_on_gpu():
+    """The headline's step structure on a 4-matrix batch: one pass covers every matrix once (the LPT queue),
+    the e2e leg declares the whole batch's copies, and the per-matrix sweeps sum to the pass."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--matrices", "4", "--steps", "1", "--warmup", "1",
+                        "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    (line,) = _json_lines(r.stdout)
+    cfg = line["config"]
+    assert cfg["matrices"] == 4 and cfg["points_per_step"] == 4 * 1024 * 1024
+    assert sorted(p["matrix"] for p in line["phases_ms"]) == [0, 1, 2, 3]
+    assert sum(p["sweep"] for p in line["phases_ms"]) == pytest.approx(line["ms_per_step"], rel=1e-3)
+    assert line["e2e"]["d2h_bytes_per_step"] == 4 * 1024 * 1024 * 9 and line["e2e"]["value"] > 0
+    assert 0 < line["roofline"]["share_of_step"] <= 1.001

@@ -369,3 +369,17 @@ def test_singularity_certificate_points_are_below_the_floor(gpu, name, count):
     check(vals[pick], ref, norm2, f"{name} certified points")
     assert ref.max() <= 1e-15 * norm2, f"{name}: certified point with reference sigma {ref.max():.3e}"
     print(f"{name}: {dec.size} certified points; sample max reference sigma {ref.max() / norm2:.2e} ||A||_2")
+
+
+@pytest.mark.parametrize("name", ["C2", "C5"])
+def test_engine_split_counts_match_the_pipeline(gpu, name):
+    """psb_engine_split (the batch scheduler's cost estimate) runs the same classification test as a sweep:
+    its counts equal the sweep's engine counts on the same points."""
+    cfg = configs.CONFIGS[name]
+    A = cfg.matrix(0)
+    zs = cfg.grid.points()[::7, ::5].ravel()
+    nb, nl = core.engine_split(A, zs)
+    core.smin_many(A, zs)
+    st = core.last_stats()
+    assert (nb, nl) == (st["n_bisect"], st["n_lanczos"]) and nb + nl == zs.size
+    assert core.engine_split(A, zs[:0]) == (0, 0)

@@ -146,3 +146,58 @@ def test_gloo_world2_matrix_batch():
     assert res[1][1] is None
     want = np.stack([np.full((3, 4), 10.0 * i) + np.arange(12).reshape(3, 4) for i in range(7)])
     assert np.array_equal(res[0][1], want)
+
+
+def _worker_dynamic(rank, world, port, q):
+    import time
+
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    costs = [3, 40, 5, 1, 22, 8, 30, 2, 2, 15, 9]
+    order = shard.lpt_order(costs)
+    mats = [np.full((2, 2), float(i)) for i in range(len(costs))]
+
+    def slow_eval(A, g):  # cost-proportional work, so the queue really interleaves the two ranks
+        time.sleep(0.01 * costs[int(A[0, 0])])
+        return float(A[0, 0]) * 10
+    got = shard.dynamic_matrix_batch(mats, None, evaluate_field=slow_eval, order=order, key="t/pass0")
+    again = shard.dynamic_matrix_batch(mats, None, evaluate_field=lambda A, g: 1.0, order=order, key="t/pass1")
+    maps = {i: np.full((3, 4), v) + np.arange(12).reshape(3, 4) for i, v in got.items()}
+    full = shard.gather_matrix_maps(maps, len(mats), (3, 4))
+    q.put((rank, (got, sorted(again), full)))
+    dist.destroy_process_group()
+
+
+def test_lpt_order_and_local_queue():
+    assert shard.lpt_order([3, 40, 5, 40, 0]) == [1, 3, 2, 0, 4]
+    c = shard.LocalCounter()
+    assert list(shard.dynamic_items([4, 2, 9], "k", c)) == [4, 2, 9]
+    assert list(shard.dynamic_items([4, 2, 9], "k", c)) == []  # the key's pass is exhausted
+    assert list(shard.dynamic_items([4, 2, 9], "k2", c)) == [4, 2, 9]
+
+
+def test_gloo_world2_dynamic_matrix_batch():
+    """C5 batches across ranks: ranks pull whole matrices from the process group's store
+    counter in LPT order; every matrix is computed exactly once, both ranks get work, each pass (key) is an
+    independent queue, and the gather reassembles any ownership in matrix order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_dynamic, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = 11
+    got = {r: v[0] for r, v in res.items()}
+    assert sorted(list(got[0]) + list(got[1])) == list(range(n))  # exactly once
+    assert got[0] and got[1]
+    assert sorted(res[0][1] + res[1][1]) == list(range(n))        # a fresh key is a fresh queue
+    assert all(v == 10 * i for part in got.values() for i, v in part.items())
+    assert res[1][2] is None
+    want = np.stack([np.full((3, 4), 10.0 * i) + np.arange(12).reshape(3, 4) for i in range(n)])
+    assert np.array_equal(res[0][2], want)
