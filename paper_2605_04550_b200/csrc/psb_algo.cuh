@@ -73,16 +73,17 @@ PSB_HD double2 crcp(double2 d) {
 
 // 1/d = conj(d) / |d|^2 with a MUFU-seeded reciprocal (about 1 ulp) when |d|^2 is safely inside
 // the normal range; Smith's scaled division otherwise.
-// Reciprocal for the LDL^H pivots: MUFU seed + two Newton steps (~1 ulp; the PD decision only
-// needs the sign of every pivot, and L = s / D is insensitive to an ulp in 1/D).
+// Reciprocal for the LDL^H pivots: MUFU seed r (relative error e = 1 - x r ~ 2^-23) refined in one
+// cubic step, 1/x = r (1 + e + e^2) (1 - e^3)^-1: three dependent FMAs instead of two Newton steps' four,
+// ~1 ulp either way (the PD decision only needs the sign of every pivot, and L = s / D is insensitive
+// to an ulp in 1/D).
 PSB_HD double fast_rcp(double x) {
 #ifdef __CUDA_ARCH__
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  const double e = fma(-x, r, 1.0);
+  const double t = fma(e, e, e);
+  return fma(r, t, r);
 #else
   return 1.0 / x;
 #endif
@@ -489,16 +490,30 @@ PSB_HD double2 g_entry(int n, int j, int d, const double2* __restrict__ Ab, doub
 }
 
 // The same entry from the expansion G = A^H A - conj(z) A - z A^H + |z|^2 I (AHA[d * n + j] =
-// (A^H A)[j, j-d], precomputed per matrix; the |z|^2 - lam diagonal term is the caller's zz). Three
-// terms per entry instead of b - d + 1 products, with rounding relative to (|z| + ||A||)^2: the form
-// of the general-band kernels, whose engine split uses that scale.
+// (A^H A)[j, j-d], precomputed per matrix; the |z|^2 - lam diagonal term is the caller's zz), with rounding
+// relative to (|z| + ||A||)^2: the form of the general-band kernels, whose engine split uses that scale.
+// With z = x + iy, a = A[j, j-d], b = A[j-d, j]:  conj(z) a + z conj(b) = x P + y Q,
+//   P = a + conj(b),  Q = i (conj(b) - a)   (z-independent; both real on the diagonal, a = b),
+// so an entry is AHA_d - x P - y Q: two real-by-complex FMAs (4 DFMA) instead of two complex ones (8).
+// g_pq forms (P, Q) exactly as psb_set_matrix packs them into the staged row table (BisRow): one rounding
+// per component, the same on the host and the device, so both paths give the same bits.
+PSB_HD void g_pq(double2 a, double2 b, double2* P, double2* Q) {
+  *P = cmk(a.x + b.x, a.y - b.y);
+  *Q = cmk(a.y + b.y, b.x - a.x);
+}
+PSB_HD double2 g_from_pq(double2 aha, double2 P, double2 Q, double2 z) {
+  return cmk(fma(-z.y, Q.x, fma(-z.x, P.x, aha.x)), fma(-z.y, Q.y, fma(-z.x, P.y, aha.y)));
+}
 template <int KLM, int KUM>
 PSB_HD double2 g_entry_aha(int n, int j, int d, const double2* __restrict__ Ab, const double2* __restrict__ AHA,
                            double2 z) {
-  double2 v = AHA[(int64_t)d * n + j];
-  if (d <= KLM) v = cfms_cj(v, z, Ab[(int64_t)(KLM - d) * n + j]);             // - conj(z) A[j, j-d]
-  if (d <= KUM) v = cfms(v, z, cconj(Ab[(int64_t)(KLM + d) * n + (j - d)]));  // - z conj(A[j-d, j])
-  return v;
+  const double2 v = AHA[(int64_t)d * n + j];
+  if (d > KLM && d > KUM) return v;
+  const double2 a = (d <= KLM) ? Ab[(int64_t)(KLM - d) * n + j] : czero();        // A[j, j-d]
+  const double2 b = (d <= KUM) ? Ab[(int64_t)(KLM + d) * n + (j - d)] : czero();  // A[j-d, j]
+  double2 P, Q;
+  g_pq(a, b, &P, &Q);
+  return g_from_pq(v, P, Q, z);
 }
 
 // One row of the factorization for static shapes, for NP independent shifts lambda_q that share

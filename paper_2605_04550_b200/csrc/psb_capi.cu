@@ -329,14 +329,22 @@ int psb_set_matrix(psb_handle* h, const double* band, int32_t n, int32_t kl, int
     CK(h->AHA.ensure(sizeof(cd) * (b + 1) * n));
     CK(cudaMemcpy(h->AHA.p, aha.data(), sizeof(cd) * (b + 1) * n, cudaMemcpyHostToDevice));
     // the same coefficients row-packed for the general-band bisection kernels (BisRow, psb_engines.cuh):
-    // row i = [AHA_d (d = 0..b) | A[i, i-d] (d = 0..kl) | A[i-d, i] (d = 1..ku)]
-    const int RW = 2 * b + 2;
+    // row i = [AHA_d (d = 0..b) | (P_0, Q_0) | P_d, Q_d (d = 1..D)], D = max(kl, ku), with
+    // P = a + conj(b), Q = i (conj(b) - a), a = A[i, i-d], b = A[i-d, i] (g_pq: plain sums, one rounding each)
+    const int Dm = std::max(kl, ku);
+    const int RW = b + 2 * Dm + 2;
     std::vector<cd> rt((size_t)RW * n, cd(0, 0));
     for (int i = 0; i < n; i++) {
       cd* row = rt.data() + (size_t)i * RW;
       for (int d = 0; d <= b; d++) row[d] = aha[(size_t)d * n + i];
-      for (int d = 0; d <= kl; d++) row[b + 1 + d] = A[(int64_t)(kl - d) * n + i];
-      for (int d = 1; d <= ku; d++) row[b + 1 + kl + d] = (i - d >= 0) ? A[(int64_t)(kl + d) * n + (i - d)] : cd(0, 0);
+      for (int d = 0; d <= Dm; d++) {
+        const cd av = (d <= kl) ? A[(int64_t)(kl - d) * n + i] : cd(0, 0);
+        const cd bv = (d <= ku && i - d >= 0) ? A[(int64_t)(kl + d) * n + (i - d)] : cd(0, 0);
+        const cd P(av.real() + bv.real(), av.imag() - bv.imag());
+        const cd Q(av.imag() + bv.imag(), bv.real() - av.real());
+        if (d == 0) row[b + 1] = cd(P.real(), Q.real());
+        else { row[b + 2 * d] = P; row[b + 2 * d + 1] = Q; }
+      }
     }
     CK(h->RT.ensure(sizeof(cd) * rt.size()));
     CK(cudaMemcpy(h->RT.p, rt.data(), sizeof(cd) * rt.size(), cudaMemcpyHostToDevice));
@@ -414,9 +422,10 @@ static double flops_ldl_row(int kl, int ku) { const double b = kl + ku; return 4
 // (8 flops each) -> 4 (b+1)(b+2) + 2 (the two diagonals of M); shared by the probes of a round, and
 // formed once per round for the interior rows of a diagonal-constant band.
 static double flops_g_row(int kl, int ku) { const double b = kl + ku; return 4.0 * (b + 1) * (b + 2) + 2.0; }
-// Forming one G row from the A^H A expansion (g_entry_aha): kl + 1 entries take - conj(z) A[j, j-d] and
-// ku + 1 take - z conj(A[j-d, j]) (one complex FMA, 8 flops, each), plus |z|^2 - lambda on the diagonal.
-static double flops_g_row_aha(int kl, int ku) { return 8.0 * (kl + 1) + 8.0 * (ku + 1) + 2.0; }
+// Forming one G row from the A^H A expansion (g_entry_aha): entry d = 1..max(kl, ku) is AHA_d - Re(z) P_d
+// - Im(z) Q_d (two real-by-complex FMAs, 8 flops), the diagonal the same with real P_0, Q_0 (4 flops), plus
+// |z|^2 - lambda on the diagonal.
+static double flops_g_row_aha(int kl, int ku) { return 8.0 * std::max(kl, ku) + 4.0 + 2.0; }
 static double flops_lu_row(int kl, int ku) { const int W = kl + ku; return 6.0 * W + 6.0 + kl * (6.0 + 8.0 * W); }
 static double flops_it_row(int kl, int ku) {
   const int W = kl + ku;

@@ -48,12 +48,14 @@ struct BisArgs {
 };
 
 // Row-packed coefficient table of the general-band G rows (psb_set_matrix): row i holds
-//   [AHA_d = (A^H A)[i, i-d], d = 0..B | A[i, i-d], d = 0..KL | A[i-d, i], d = 1..KU]
-// so G[i, i-d] = AHA_d - conj(z) A[i, i-d] - z conj(A[i-d, i]) (g_entry_aha) reads one contiguous span.
+//   [AHA_d = (A^H A)[i, i-d], d = 0..B | (P_0, Q_0) (both real) | P_d, Q_d, d = 1..D],  D = max(KL, KU),
+// with P_d = a + conj(b), Q_d = i (conj(b) - a), a = A[i, i-d], b = A[i-d, i] (g_pq, psb_algo.cuh), so
+// G[i, i-d] = AHA_d - Re(z) P_d - Im(z) Q_d (g_entry_aha) reads one contiguous span.
 template <int KL, int KU>
 struct BisRow {
   static constexpr int B = KL + KU;
-  static constexpr int RW = 2 * B + 2;  // complex per row
+  static constexpr int D = KL > KU ? KL : KU;
+  static constexpr int RW = B + 2 * D + 2;  // complex per row
   static constexpr int RB = 8;          // rows per stage (one unrolled block of the row loop)
   static constexpr int SE = RB * RW;    // complex per stage
   static constexpr int BYTES = 2 * SE * 16;  // two stages per warp
@@ -625,8 +627,12 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
             g[d] = czero();
             if (i < a.n && i - d >= 0) {
               double2 v = row[d];
-              if (d <= KL) v = cfms_cj(v, zt, row[B + 1 + d]);                           // - conj(z) A[i, i-d]
-              if (d <= KU) v = cfms(v, zt, cconj(d == 0 ? row[B + 1] : row[B + 1 + KL + d]));  // - z conj(A[i-d, i])
+              if (d == 0) {  // diagonal: P_0, Q_0 are real and share one slot
+                const double2 pq = row[B + 1];
+                v.x = fma(-zt.y, pq.y, fma(-zt.x, pq.x, v.x));
+              } else if (d <= BR::D) {
+                v = g_from_pq(v, row[B + 2 * d], row[B + 2 * d + 1], zt);
+              }
               g[d] = v;
             }
           }

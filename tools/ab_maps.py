@@ -61,6 +61,10 @@ for m in mats:
         dm = a != b
         print(f"  changed points: max |diff| / max_j ||A e_j|| = {np.max(np.abs(a - b)[dm]) / cmax:.2e}, "
               f"A-side values there <= {np.max(a[dm]) / cmax:.2e} ||A e_j||, B-side <= {np.max(b[dm]) / cmax:.2e}")
+    if nd:
+        rel = np.abs(a - b) / np.maximum(np.abs(a), 1e-300)
+        k = int(np.nanargmax(rel))
+        print(f"  largest relative change at flat index {k}: A {a.ravel()[k]:.6e}  B {b.ravel()[k]:.6e}")
     ta, tb = res["a"][str(m)], res["b"][str(m)]
     print(f"{name} m={m}: bitwise {eq} (max rel {d:.2e}, {nd} differ, max|diff|/max {dabs:.1e}) | A total {ta['ms_total']:.1f} B {ta['ms_bisect']:.1f} "
           f"L {ta['ms_lanczos']:.1f} C {ta.get('ms_classify', 0):.1f} | B total {tb['ms_total']:.1f} "
