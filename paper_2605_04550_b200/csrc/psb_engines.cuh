@@ -620,27 +620,24 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           }
           cp_commit();
         };
+        // Staged rows need no edge tests: i >= B + 1, so every column i - d exists, and rows past n are
+        // zero-filled by the copy, so their entries come out zero; only the diagonal picks the identity
+        // padding (PD-neutral) there.
         auto load_staged = [&](const double2* row, int i) {
           double2 g[B + 1];
+          const double2 pq = row[B + 1];  // diagonal: P_0, Q_0 are real and share one slot
+          const double g0 = fma(-zt.y, pq.y, fma(-zt.x, pq.x, row[0].x));
 #pragma unroll
-          for (int d = 0; d <= B; d++) {
-            g[d] = czero();
-            if (i < a.n && i - d >= 0) {
-              double2 v = row[d];
-              if (d == 0) {  // diagonal: P_0, Q_0 are real and share one slot
-                const double2 pq = row[B + 1];
-                v.x = fma(-zt.y, pq.y, fma(-zt.x, pq.x, v.x));
-              } else if (d <= BR::D) {
-                v = g_from_pq(v, row[B + 2 * d], row[B + 2 * d + 1], zt);
-              }
-              g[d] = v;
-            }
+          for (int d = 1; d <= B; d++) {
+            double2 v = row[d];
+            if (d <= BR::D) v = g_from_pq(v, row[B + 2 * d], row[B + 2 * d + 1], zt);
+            g[d] = v;
           }
 #pragma unroll
           for (int q = 0; q < NP; q++) {
 #pragma unroll
-            for (int c = 0; c <= B; c++) Wn[q].W[B][c] = g[B - c];
-            Wn[q].W[B][B].x += (i < a.n) ? zz[q] : 1.0;
+            for (int c = 0; c < B; c++) Wn[q].W[B][c] = g[B - c];
+            Wn[q].W[B][B].x = (i < a.n) ? g0 + zz[q] : 1.0;
             Wn[q].W[B][B].y = 0.0;
           }
         };

@@ -43,7 +43,7 @@ for tag, spec in (("a", la), ("b", lb)):
 for m in mats:
     a, b = np.load(f"/tmp/ab_a_{m}.npy"), np.load(f"/tmp/ab_b_{m}.npy")
     eq = np.array_equal(a, b)
-    d = np.max(np.abs(a - b) / np.maximum(np.abs(a), 1e-300))
+    relmax = np.max(np.abs(a - b) / np.maximum(np.abs(a), 1e-300))
     nd = int(np.sum(a != b))
     dabs = float(np.max(np.abs(a - b))) / float(np.max(a))  # largest change against the map's scale
     if nd:
@@ -66,6 +66,6 @@ for m in mats:
         k = int(np.nanargmax(rel))
         print(f"  largest relative change at flat index {k}: A {a.ravel()[k]:.6e}  B {b.ravel()[k]:.6e}")
     ta, tb = res["a"][str(m)], res["b"][str(m)]
-    print(f"{name} m={m}: bitwise {eq} (max rel {d:.2e}, {nd} differ, max|diff|/max {dabs:.1e}) | A total {ta['ms_total']:.1f} B {ta['ms_bisect']:.1f} "
+    print(f"{name} m={m}: bitwise {eq} (max rel {relmax:.2e}, {nd} differ, max|diff|/max {dabs:.1e}) | A total {ta['ms_total']:.1f} B {ta['ms_bisect']:.1f} "
           f"L {ta['ms_lanczos']:.1f} C {ta.get('ms_classify', 0):.1f} | B total {tb['ms_total']:.1f} "
           f"B {tb['ms_bisect']:.1f} L {tb['ms_lanczos']:.1f} C {tb.get('ms_classify', 0):.1f} ms")
