@@ -86,6 +86,8 @@ struct psb_handle {
   double k_cert_delta = 1e-16;  // PSB_CERT_DELTA=x (0: certificates off, the round-2 overflow rule alone)
   bool k_bexpand = true, k_fallback = true, k_seq = false;
   int k_bvariant = 0;
+  double k_lfrac = 0.5;
+  int k_bfull = 1;
   struct FitEntry { const void* f; int lkey, btpb, tpb, occ, occFull; int64_t threads; int wregs; };
   std::vector<FitEntry> fit_cache;  // engine-B launch shapes per (kernel, engine-L share)
   struct LanEntry { const void* f; int lsmem, occ, regs; };
@@ -197,6 +199,8 @@ int psb_create(int device, psb_handle** out) {
   h->k_tau = getenv("PSB_TAU") ? atof(getenv("PSB_TAU")) : 0.0;  // dev: default engine split
   h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 0;  // 0: pick per launch
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
+  h->k_lfrac = getenv("PSB_LFRAC") ? atof(getenv("PSB_LFRAC")) : 0.5;   // dev: SM share hosting an engine-L block (long general lists)
+  h->k_bfull = getenv("PSB_BFULL") ? atoi(getenv("PSB_BFULL")) : 1;     // dev: 0 restores the two-launch engine B on long general lists
   h->k_refill = getenv("PSB_REFILL") ? atoi(getenv("PSB_REFILL")) : 16;  // dev: engine-L refill threshold
   h->k_cert_delta = getenv("PSB_CERT_DELTA") ? atof(getenv("PSB_CERT_DELTA")) : 1e-16;
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -548,6 +552,16 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   // 4.3 ms) because every SM then hosts more engine-L warps next to the FP64-bound bisection warps.
   constexpr int kLWarpsPerBlock = 4;
   const int lsmem = kp.lsmem * kLWarpsPerBlock;
+  // Long general-band lists (C5): engine B is the long pole (FP64-bound, ~1.3 us per point against ~0.2 us for
+  // engine L's, most of which a certificate decides early), and two engine-L blocks leave an SM no room for
+  // a bisection warp. Engine L then takes one block on half of the SMs (1.8x its time with every SM, so it
+  // stays the shorter engine while 3 nB >= nA, i.e. engine B's estimate is twice engine L's), and engine B
+  // is one launch of its full-occupancy grid: its blocks fill the SMs engine L left free at once and the
+  // rest as engine L's blocks retire. Launch shape only: the same bits. C5 matrices 0/4/12/42/10:
+  // 483/522/548/918/645 -> 449/496/527/903/629 ms (a third of the SMs: 442/484/524/900/625, but matrix 4's
+  // engine L then ends 17 ms before engine B; every SM: 471/521/549/920/648).
+  const bool long_general = bsw > 0 && nA > 0 && h->k_bfull && !h->k_seq &&
+                            nB >= (int64_t)1024 * h->num_sms && 3 * nB >= nA;
   int64_t gridL = 0;
   int occL = 0;
   if (nA > 0) {
@@ -569,6 +583,8 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     int64_t warps = std::min<int64_t>((int64_t)occL * h->num_sms * kLWarpsPerBlock, (nA + 31) / 32);
     warps = std::min<int64_t>(warps, (int64_t)(budget / per_warp));
     if (h->k_lwarps > 0) warps = std::min<int64_t>(warps, h->k_lwarps);
+    if (long_general)
+      warps = std::min<int64_t>(warps, std::max<int64_t>(1, (int64_t)(h->k_lfrac * h->num_sms + 0.5)) * kLWarpsPerBlock);
     warps = std::max<int64_t>(kLWarpsPerBlock, (warps + kLWarpsPerBlock - 1) / kLWarpsPerBlock * kLWarpsPerBlock);
     gridL = warps / kLWarpsPerBlock;
     CK(h->scratch.ensure((size_t)(warps * warp_stride * sizeof(double2))));
@@ -666,7 +682,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     const int64_t wantB = (nB * kp.g + tpbB - 1) / tpbB;
     gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occShare * h->num_sms, wantB));
     const bool seq = h->k_seq && nA > 0 && gridL > 0;
-    if (seq) gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occFull * h->num_sms, wantB));
+    if (seq || long_general) gridB = std::max<int64_t>(1, std::min<int64_t>((int64_t)occFull * h->num_sms, wantB));
     // A second launch, queued behind engine L on its stream, takes the SM share engine L releases when
     // it finishes (both launches pull from the same work counter), so a long bisection tail runs at
     // full occupancy instead of the share it had next to engine L.
@@ -674,7 +690,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     // late starters' last points stretch the tail by a point's latency (C3: +4%; C5: -15%).
     bis_fn fB2 = kp.bm;
     int tpb2 = tpbB, g2 = kp.g;
-    if (nA > 0 && gridL > 0 && h->k_bexpand && !seq) {
+    if (nA > 0 && gridL > 0 && h->k_bexpand && !seq && !long_general) {
       const int64_t extra = std::max<int64_t>(0, std::min<int64_t>((int64_t)occFull * h->num_sms, wantB) - gridB);
       if (nB * kp.g >= 4 * (gridB + extra) * tpbB) {
         gridB2 = extra;  // long list: the same (wide) variant at full occupancy (C5 1157 -> 975 ms)
