@@ -99,7 +99,7 @@ struct psb_handle {
   DevBuf xs, ys, prof;
   PinBuf pin;
   // predictor
-  DevBuf params, feat, eig, prob, region, idx, selblk;
+  DevBuf params, feat, eig, prob, region, idx, selblk, g13;
   // current device selection (psb_region_select / the region path): h->outidx[0, sel_P) of an sel_N grid
   bool sel_valid = false;
   int64_t sel_N = 0, sel_P = 0;
@@ -215,7 +215,7 @@ void psb_destroy(psb_handle* h) {
   DeviceGuard dg(h->device);
   DevBuf* bufs[] = {&h->Ab, &h->AHA, &h->RT, &h->LUT, &h->v1, &h->offmin, &h->gbuf, &h->listF, &h->zs, &h->outidx, &h->out, &h->iters, &h->status, &h->listA, &h->listB,
                     &h->counters, &h->scratch, &h->pivs, &h->dynL, &h->dynD, &h->xs, &h->ys, &h->params,
-                    &h->feat, &h->eig, &h->prob, &h->region, &h->idx, &h->selblk};
+                    &h->feat, &h->eig, &h->prob, &h->region, &h->idx, &h->selblk, &h->g13};
   for (DevBuf* b : bufs) b->release();
   h->pin.release();
   for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
@@ -1117,6 +1117,10 @@ int psb_predict_points(psb_handle* h, const double* params, const double* mean33
   a.zs = h->zs.as<double2>();
   a.P = P;
   a.prob = h->prob.as<double>();
+  CK(h->g13.ensure(sizeof(double) * 2 * P));
+  a.g13 = h->g13.as<double>();
+  k_point_features<<<(unsigned)((P + 127) / 128), 128, 0, st>>>(a);
+  CK(cudaGetLastError());
   const size_t smem = sizeof(double) * 3 * 128 * MLP_TPB;
   CK(cudaFuncSetAttribute(k_predict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = (P + MLP_TPB - 1) / MLP_TPB;

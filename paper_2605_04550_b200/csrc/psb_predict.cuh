@@ -72,27 +72,29 @@ __device__ double np_pairwise(F f, int lo, int len) {
   return ret;
 }
 
-// y[o] = act(b[o] + sum_i W[o, i] x[i]): four outputs per pass, so four independent FMA chains are in
-// flight (one chain per output was latency-bound at two warps per SM); each output keeps its own
-// sequential sum order, so the values do not change.
+// y[o] = act(b[o] + sum_i W[o, i] x[i]): eight outputs per pass, so eight independent FMA chains are in
+// flight (one chain per output was latency-bound at two warps per SM; every layer's width is a multiple
+// of 8); each output keeps its own sequential sum order, so the values do not change.
 __device__ __forceinline__ void dense(const double* __restrict__ W, const double* __restrict__ bvec, int nin,
                                       int nout, const double* x, double* y, bool act) {
   const int t = threadIdx.x;
+  constexpr int C = 8;
   int o = 0;
-  for (; o + 4 <= nout; o += 4) {
+  for (; o + C <= nout; o += C) {
     const double* w = W + (int64_t)o * nin;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double acc[C];
+#pragma unroll
+    for (int k = 0; k < C; k++) acc[k] = 0.0;
     for (int i = 0; i < nin; i++) {
       const double xi = x[i * MLP_TPB + t];
-      a0 = fma(__ldg(w + i), xi, a0);
-      a1 = fma(__ldg(w + nin + i), xi, a1);
-      a2 = fma(__ldg(w + 2 * nin + i), xi, a2);
-      a3 = fma(__ldg(w + 3 * nin + i), xi, a3);
-    }
-    const double acc[4] = {a0 + __ldg(bvec + o), a1 + __ldg(bvec + o + 1), a2 + __ldg(bvec + o + 2),
-                           a3 + __ldg(bvec + o + 3)};
 #pragma unroll
-    for (int k = 0; k < 4; k++) y[(o + k) * MLP_TPB + t] = act ? acc[k] * expit_d(acc[k]) : acc[k];
+      for (int k = 0; k < C; k++) acc[k] = fma(__ldg(w + k * nin + i), xi, acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < C; k++) {
+      const double v = acc[k] + __ldg(bvec + o + k);
+      y[(o + k) * MLP_TPB + t] = act ? v * expit_d(v) : v;
+    }
   }
   for (; o < nout; o++) {
     const double* w = W + (int64_t)o * nin;
@@ -114,7 +116,28 @@ struct PredictArgs {
   const double2* zs;
   int64_t P;
   double* prob;
+  double* g13;  // per point: g1 = min |z - lambda|, g3 = mean |z - lambda| (k_point_features)
 };
+
+// Per-point spectral features g1, g3 (features.py:129-137): two passes over the n eigenvalues per point,
+// more than half of the predictor's instructions at n = 2000. They need no shared memory, so they run as
+// their own full-occupancy kernel (k_predict's 96 KB of activations per warp allow two warps per SM);
+// every lane of a warp reads the same eigenvalue (broadcast). The same arithmetic as before the split.
+__global__ void __launch_bounds__(128) k_point_features(PredictArgs a) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.P) return;
+  const double2 z = a.zs[p];
+  double g1 = INFINITY;
+  for (int k = 0; k < a.n_eig; k++) {
+    const double2 l = a.eig[k];
+    const double d = hypot(z.x - l.x, z.y - l.y);
+    g1 = fmin(g1, d);
+  }
+  auto dist = [&](int k) { const double2 l = a.eig[k]; return hypot(z.x - l.x, z.y - l.y); };
+  const double g3 = np_pairwise(dist, 0, a.n_eig) / (double)a.n_eig;
+  a.g13[2 * p] = g1;
+  a.g13[2 * p + 1] = g3;
+}
 
 __global__ void __launch_bounds__(MLP_TPB) k_predict(PredictArgs a) {
   extern __shared__ double sm[];
@@ -125,16 +148,10 @@ __global__ void __launch_bounds__(MLP_TPB) k_predict(PredictArgs a) {
   const int64_t p = (int64_t)blockIdx.x * MLP_TPB + t;
   const bool live = p < a.P;
   const double2 z = live ? a.zs[p] : czero();
-  // ---- features (features.py:129-137) ----
-  double g1 = INFINITY;
-  for (int k = 0; k < a.n_eig; k++) {
-    const double2 l = a.eig[k];
-    const double d = hypot(z.x - l.x, z.y - l.y);
-    g1 = fmin(g1, d);
-  }
+  // ---- features (features.py:129-137): g1, g3 from k_point_features ----
+  const double g1 = live ? a.g13[2 * p] : 0.0;
+  const double g3 = live ? a.g13[2 * p + 1] : 0.0;
   const double g2 = hypot(z.x - a.eig_mean.x, z.y - a.eig_mean.y);
-  auto dist = [&](int k) { const double2 l = a.eig[k]; return hypot(z.x - l.x, z.y - l.y); };
-  const double g3 = np_pairwise(dist, 0, a.n_eig) / (double)a.n_eig;
   // standardized 33-vector into Z[0..32]
   for (int c = 0; c < 30; c++) Z[c * MLP_TPB + t] = (a.f30[c] - a.mean33[c]) / a.std33[c];
   Z[30 * MLP_TPB + t] = (g1 - a.mean33[30]) / a.std33[30];
