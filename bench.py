@@ -558,6 +558,9 @@ def run_ours(args, rank, world, local_rank):
     ms_local = float(np.mean(step_ms))
     assert roof["ms"] <= ms_local * 1.001 + 1e-3, f"kernel window {roof['ms']} ms > step {ms_local} ms"
     roof["share_of_step"] = roof["ms"] / ms_local
+    # the engines overlap inside a step, so their windows sum to more than the step; ncu serialises them:
+    # the window's share of the summed windows is the figure to hold against profiles/*_launches.csv
+    roof["share_of_serialised_kernels"] = roof["ms"] / max(1e-12, sum(k["ms"] for k in kerns.values()))
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
@@ -570,6 +573,7 @@ def run_ours(args, rank, world, local_rank):
     flops_pt = (S["flops_bisect"] + S["flops_lanczos"] + S["flops_classify"]) / max(1, S["n_points"])
     roof_pts = fp64_peak * 1e12 / flops_pt if flops_pt > 0 else None
     model = lu_solve_model(n_, kl_, ku_, S, fp64_peak, hbm_peak)
+    model["frac_of_roof"] = value / (model["roof_points_per_s_per_gpu"] * world)
 
     guided = None
     if rank == 0 and world == 1 and name in ("C1", "C2", "C4") and not args.no_guided:

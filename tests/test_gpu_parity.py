@@ -326,6 +326,32 @@ def test_randomised_band_sweep(gpu):
         check(core.smin_many(A, zs), smin_restated(A, zs), np.linalg.norm(A, 2), f"sweep case {t} n={n} ({kl},{ku}) {kind}")
 
 
+@pytest.mark.parametrize("kl,ku", [(3, 3), (1, 3), (2, 1)])
+def test_general_band_rows_every_remainder(gpu, kl, ku):
+    """General-band bisection kernels (noisy bands: no diagonal-constant interior): G rows come from the
+    staged row table in the form AHA - Re(z) P - Im(z) Q in 8-row blocks, from the band itself for the first
+    kl + ku + 1 rows and for the n mod 8 rows after the last block, and rows past n are zero-filled stage
+    rows. Every remainder n mod 8 and sizes below one block, bisection forced on every point (shifts well
+    outside the spectrum, where the squared form is accurate), against zgesdd."""
+    from oracle.sigma_oracle import smin_restated
+    rng = np.random.default_rng(7 * kl + ku)
+    worst = 0.0
+    for n in (7, 9, 15, 16, 17, 64, 66, 67, 68, 69, 70, 71, 133):
+        c = (rng.standard_normal(kl + ku + 1) + 1j * rng.standard_normal(kl + ku + 1))
+        A = np.zeros((n, n), complex)
+        for d in range(-kl, ku + 1):
+            m = n - abs(d)
+            A += np.diag(np.full(m, c[d + kl]) + 1e-3 * (rng.standard_normal(m) + 1j * rng.standard_normal(m)), d)
+        r = np.abs(c).sum()
+        ang = rng.uniform(0, 2 * np.pi, 10)
+        zs = (1.3 + rng.uniform(0, 1.0, 10)) * r * np.exp(1j * ang)
+        got, it, st = core.smin_many(A, zs, opts=_lib.make_opts(force_engine=2), return_info=True)
+        assert (st == 1).all(), (n, st)
+        worst = max(worst, check(got, smin_restated(A, zs), np.linalg.norm(A, 2), f"general ({kl},{ku}) n={n}"))
+        assert np.array_equal(got, core.smin_many(A, zs, opts=_lib.make_opts(force_engine=2)))
+    print(f"[general-band rows ({kl},{ku})] worst floored rel err {worst:.2e}")
+
+
 @pytest.mark.parametrize("name", ["C1", "C3"])
 def test_engine_b_variants_bitwise_equal(gpu, tmp_path, name):
     """The wide (NP = 2) and pair (NP = 1, G = 2) bisection variants probe the same shifts with the same
