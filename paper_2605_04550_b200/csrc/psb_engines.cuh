@@ -342,7 +342,8 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
 }
 
 // cp.async ring depth (rows in flight + 1): 16 for tridiagonal bands, 8 otherwise, 4 for (3,3). Measured on
-// B200: C4 (1,1) 425 -> 400 ms at 16; C2 (1,3) 3.26 -> 3.45 ms at 13, so wider bands keep 8 (at 4: C2
+// B200: C4 (1,1) 425 -> 400 ms at 16 (end of round 2, where shallower rings would fit two blocks per SM:
+// 81.6 ms at 16, 84.8 / 89.7 / 103.8 ms at 8 / 6 / 4 - the kernel is HBM-bound, more warps do not help); C2 (1,3) 3.26 -> 3.45 ms at 13, so wider bands keep 8 (at 4: C2
 // 2.3 -> 2.4, C3 14.9 -> 15.1 ms). (3,3) (C5, whose engine-L points are mostly LU-bound) at 4: the
 // per-warp ring drops from 42 to 21 KB, so two engine-L blocks fit an SM: C5 matrices 0/1/17/63
 // 813/326/709/452 -> 747/302/615/411 ms (depth 3: within 1%).
@@ -352,9 +353,12 @@ __device__ double pl_s4(int n, const Ring<KL, KU, D>& R, LV FU, LV T, LV RA, dou
 #ifndef PSB_DW
 #define PSB_DW 8
 #endif
+#ifndef PSB_D11
+#define PSB_D11 16
+#endif
 template <int KL, int KU>
 struct RingDepth {
-  static constexpr int D = (KL + KU <= 2) ? 16 : (KL == 3 && KU == 3 ? PSB_D33 : PSB_DW);
+  static constexpr int D = (KL + KU <= 2) ? PSB_D11 : (KL == 3 && KU == 3 ? PSB_D33 : PSB_DW);
 };
 
 __device__ __forceinline__ int64_t out_index(const int64_t* outidx, int64_t p) { return outidx ? outidx[p] : p; }
