@@ -1121,9 +1121,9 @@ int psb_predict_points(psb_handle* h, const double* params, const double* mean33
   a.g13 = h->g13.as<double>();
   k_point_features<<<(unsigned)((P + 127) / 128), 128, 0, st>>>(a);
   CK(cudaGetLastError());
-  const size_t smem = sizeof(double) * 3 * 128 * MLP_TPB;
+  const size_t smem = MLP_SMEM;
   CK(cudaFuncSetAttribute(k_predict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t grid = (P + MLP_TPB - 1) / MLP_TPB;
+  const int64_t grid = (P + MLP_PB - 1) / MLP_PB;
   k_predict<<<(unsigned)grid, MLP_TPB, smem, st>>>(a);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(prob, h->prob.p, sizeof(double) * P, cudaMemcpyDeviceToHost, st));

@@ -9,9 +9,9 @@
 //   region               pseudospec/pipeline.py:227-231 predicted_region: dilate(prob >= tau, 5)
 //                        with border clipping (core.py:224-231, scipy binary_dilation)
 //
-// FP64 throughout (the reference network is float64, network.py:1-14). One thread per point;
-// weights are read with warp-uniform addresses (broadcast), activations live in shared
-// memory interleaved by thread ([unit][thread]) so the per-thread reads are bank-conflict free.
+// FP64 throughout (the reference network is float64, network.py:1-14). Four lanes per point, each
+// taking a quarter of a layer's outputs; weights are read with four addresses per warp (one per lane
+// of a group), activations live in shared memory interleaved by point ([unit][point slot]).
 #pragma once
 #include "psb_algo.cuh"
 
@@ -27,7 +27,16 @@ struct MlpOff {
 };
 static_assert(MlpOff::total == 59841, "PARAM_SHAPES total");
 
-constexpr int MLP_TPB = 32;  // threads per block (one warp): smem = 3 * 128 * 32 * 8 = 96 KB
+// Four warps share 32 points: lane = point, and warp w computes the outputs o = 4 m + w of every layer, so
+// a 128-thread block holds 32 points and its activations (two 128-wide buffers + the three per-point
+// features) take 66 KB: three blocks = 12 warps per SM, and every weight load is one warp-uniform
+// (broadcast) address. (One thread per point with three 128-wide buffers needed 96 KB per warp: two warps
+// per SM. Four *lanes* per point gave the same occupancy but four addresses per weight load: the LSU's
+// wavefronts then bound the kernel, 3.9 ms for 65,536 points.)
+constexpr int MLP_TPB = 128;  // threads per block
+constexpr int MLP_GL = 4;     // warps per point group (output split)
+constexpr int MLP_PB = MLP_TPB / MLP_GL;  // points per block
+constexpr size_t MLP_SMEM = sizeof(double) * ((size_t)(2 * 128 + 3) * MLP_PB + 32);
 
 __device__ __forceinline__ double expit_d(double x) { return 1.0 / (1.0 + exp(-x)); }
 
@@ -72,36 +81,31 @@ __device__ double np_pairwise(F f, int lo, int len) {
   return ret;
 }
 
-// y[o] = act(b[o] + sum_i W[o, i] x[i]): eight outputs per pass, so eight independent FMA chains are in
-// flight (one chain per output was latency-bound at two warps per SM; every layer's width is a multiple
-// of 8); each output keeps its own sequential sum order, so the values do not change.
+// y[o] = act(b[o] + sum_i W[o, i] x[i]) for the block's 32 points: warp gl takes the outputs o = 4 m + gl
+// in passes of eight, so eight independent FMA chains are in flight per lane (every layer's width is a
+// multiple of 32). Each output keeps its own sequential sum over i (network.py:87-92's fixed per-row
+// order), so the values do not depend on how the outputs are split. `xin(i)` reads input i of the
+// lane's point; outputs go to y[o * MLP_PB + ps]. The caller separates layers with __syncthreads().
+template <class XIn>
 __device__ __forceinline__ void dense(const double* __restrict__ W, const double* __restrict__ bvec, int nin,
-                                      int nout, const double* x, double* y, bool act) {
-  const int t = threadIdx.x;
+                                      int nout, XIn xin, double* y, int ps, int gl, bool act) {
   constexpr int C = 8;
-  int o = 0;
-  for (; o + C <= nout; o += C) {
-    const double* w = W + (int64_t)o * nin;
+  for (int m0 = 0; m0 * MLP_GL < nout; m0 += C) {
     double acc[C];
+    const double* w[C];
 #pragma unroll
-    for (int k = 0; k < C; k++) acc[k] = 0.0;
+    for (int k = 0; k < C; k++) { acc[k] = 0.0; w[k] = W + (int64_t)((m0 + k) * MLP_GL + gl) * nin; }
     for (int i = 0; i < nin; i++) {
-      const double xi = x[i * MLP_TPB + t];
+      const double xi = xin(i);
 #pragma unroll
-      for (int k = 0; k < C; k++) acc[k] = fma(__ldg(w + k * nin + i), xi, acc[k]);
+      for (int k = 0; k < C; k++) acc[k] = fma(__ldg(w[k] + i), xi, acc[k]);
     }
 #pragma unroll
     for (int k = 0; k < C; k++) {
-      const double v = acc[k] + __ldg(bvec + o + k);
-      y[(o + k) * MLP_TPB + t] = act ? v * expit_d(v) : v;
+      const int o = (m0 + k) * MLP_GL + gl;
+      const double v = acc[k] + __ldg(bvec + o);
+      y[o * MLP_PB + ps] = act ? v * expit_d(v) : v;
     }
-  }
-  for (; o < nout; o++) {
-    const double* w = W + (int64_t)o * nin;
-    double acc = 0.0;
-    for (int i = 0; i < nin; i++) acc = fma(__ldg(w + i), x[i * MLP_TPB + t], acc);
-    acc += __ldg(bvec + o);
-    y[o * MLP_TPB + t] = act ? acc * expit_d(acc) : acc;
   }
 }
 
@@ -141,48 +145,66 @@ __global__ void __launch_bounds__(128) k_point_features(PredictArgs a) {
 
 __global__ void __launch_bounds__(MLP_TPB) k_predict(PredictArgs a) {
   extern __shared__ double sm[];
-  double* X = sm;                       // 128 x TPB
-  double* Y = sm + 128 * MLP_TPB;       // 128 x TPB
-  double* Z = sm + 256 * MLP_TPB;       // 128 x TPB
+  double* X = sm;                        // 128 x PB
+  double* Y = sm + 128 * MLP_PB;         // 128 x PB
+  double* Zp = sm + 256 * MLP_PB;        // 3 x PB: the standardized per-point features g1, g2, g3
+  double* Zc = sm + 259 * MLP_PB;        // 30: the standardized per-matrix features (the same for every point)
   const int t = threadIdx.x;
-  const int64_t p = (int64_t)blockIdx.x * MLP_TPB + t;
+  const int gl = t >> 5;                 // warp: which quarter of a layer's outputs
+  const int ps = t & 31;                 // point slot in the block (lane)
+  const int64_t p = (int64_t)blockIdx.x * MLP_PB + ps;
   const bool live = p < a.P;
   const double2 z = live ? a.zs[p] : czero();
-  // ---- features (features.py:129-137): g1, g3 from k_point_features ----
-  const double g1 = live ? a.g13[2 * p] : 0.0;
-  const double g3 = live ? a.g13[2 * p + 1] : 0.0;
-  const double g2 = hypot(z.x - a.eig_mean.x, z.y - a.eig_mean.y);
-  // standardized 33-vector into Z[0..32]
-  for (int c = 0; c < 30; c++) Z[c * MLP_TPB + t] = (a.f30[c] - a.mean33[c]) / a.std33[c];
-  Z[30 * MLP_TPB + t] = (g1 - a.mean33[30]) / a.std33[30];
-  Z[31 * MLP_TPB + t] = (g2 - a.mean33[31]) / a.std33[31];
-  Z[32 * MLP_TPB + t] = (g3 - a.mean33[32]) / a.std33[32];
-  // Fourier encoding (network.py:62-75) into X[0..25]
-  X[0 * MLP_TPB + t] = z.x;
-  X[1 * MLP_TPB + t] = z.y;
-  for (int q = 0; q < 6; q++) {
-    const double f = (double)(2 << q);
-    X[(2 + 4 * q) * MLP_TPB + t] = sin(f * z.x);
-    X[(3 + 4 * q) * MLP_TPB + t] = sin(f * z.y);
-    X[(4 + 4 * q) * MLP_TPB + t] = cos(f * z.x);
-    X[(5 + 4 * q) * MLP_TPB + t] = cos(f * z.y);
+  if (t < 30) Zc[t] = (a.f30[t] - a.mean33[t]) / a.std33[t];
+  if (gl == 0) {
+    // ---- features (features.py:129-137): g1, g3 from k_point_features ----
+    const double g1 = live ? a.g13[2 * p] : 0.0;
+    const double g3 = live ? a.g13[2 * p + 1] : 0.0;
+    const double g2 = hypot(z.x - a.eig_mean.x, z.y - a.eig_mean.y);
+    Zp[0 * MLP_PB + ps] = (g1 - a.mean33[30]) / a.std33[30];
+    Zp[1 * MLP_PB + ps] = (g2 - a.mean33[31]) / a.std33[31];
+    Zp[2 * MLP_PB + ps] = (g3 - a.mean33[32]) / a.std33[32];
+    // Fourier encoding (network.py:62-75) into X[0..25]
+    X[0 * MLP_PB + ps] = z.x;
+    X[1 * MLP_PB + ps] = z.y;
+    for (int q = 0; q < 6; q++) {
+      const double f = (double)(2 << q);
+      X[(2 + 4 * q) * MLP_PB + ps] = sin(f * z.x);
+      X[(3 + 4 * q) * MLP_PB + ps] = sin(f * z.y);
+      X[(4 + 4 * q) * MLP_PB + ps] = cos(f * z.x);
+      X[(5 + 4 * q) * MLP_PB + ps] = cos(f * z.y);
+    }
   }
+  __syncthreads();  // Zc is shared by the block
   const double* P = a.params;
   typedef MlpOff O;
-  // coordinate path: phi(26) -> 64 -> 64 ; h_c1 in Y[0..63], h_c2 into Y[64..127]? keep layout h3 = [h_c2, h_m2]
-  dense(P + O::w_c1, P + O::b_c1, 26, 64, X, Y, true);           // Y = h_c1
-  dense(P + O::w_c2, P + O::b_c2, 64, 64, Y, X, true);           // X[0..63] = h_c2
+  auto inX = [&](int i) { return X[i * MLP_PB + ps]; };
+  auto inY = [&](int i) { return Y[i * MLP_PB + ps]; };
+  auto inZ = [&](int i) { return i < 30 ? Zc[i] : Zp[(i - 30) * MLP_PB + ps]; };
+  // coordinate path: phi(26) -> 64 -> 64
+  dense(P + O::w_c1, P + O::b_c1, 26, 64, inX, Y, ps, gl, true);            // Y[0..63] = h_c1
+  __syncthreads();
+  dense(P + O::w_c2, P + O::b_c2, 64, 64, inY, X, ps, gl, true);            // X[0..63] = h_c2
+  __syncthreads();
   // matrix path: f(33) -> 128 -> 64
-  dense(P + O::w_m1, P + O::b_m1, 33, 128, Z, Y, true);          // Y = h_m1
-  dense(P + O::w_m2, P + O::b_m2, 128, 64, Y, X + 64 * MLP_TPB, true);  // X[64..127] = h_m2  => X = h3
-  dense(P + O::w_t1, P + O::b_t1, 128, 128, X, Y, true);         // Y = h4
-  dense(P + O::w_t2, P + O::b_t2, 128, 128, Y, Z, true);         // Z = h5
-  for (int c = 0; c < 128; c++) Z[c * MLP_TPB + t] = Y[c * MLP_TPB + t] + Z[c * MLP_TPB + t];  // h6 = h4 + h5
-  dense(P + O::w_proj, P + O::b_proj, 128, 64, Z, X, true);      // X[0..63] = h7
-  double logit = 0.0;
-  for (int i = 0; i < 64; i++) logit = fma(__ldg(P + O::w_head + i), X[i * MLP_TPB + t], logit);
-  logit += __ldg(P + O::b_head);
-  if (live) a.prob[p] = expit_d(logit);
+  dense(P + O::w_m1, P + O::b_m1, 33, 128, inZ, Y, ps, gl, true);           // Y = h_m1
+  __syncthreads();
+  dense(P + O::w_m2, P + O::b_m2, 128, 64, inY, X + 64 * MLP_PB, ps, gl, true);  // X[64..127] = h_m2  => X = h3
+  __syncthreads();
+  dense(P + O::w_t1, P + O::b_t1, 128, 128, inX, Y, ps, gl, true);          // Y = h4
+  __syncthreads();
+  dense(P + O::w_t2, P + O::b_t2, 128, 128, inY, X, ps, gl, true);          // X = h5 (h3 is dead)
+  __syncthreads();
+  for (int c = gl; c < 128; c += MLP_GL) X[c * MLP_PB + ps] = Y[c * MLP_PB + ps] + X[c * MLP_PB + ps];  // h6 = h4 + h5
+  __syncthreads();
+  dense(P + O::w_proj, P + O::b_proj, 128, 64, inX, Y, ps, gl, true);       // Y[0..63] = h7
+  __syncthreads();
+  if (gl == 0) {
+    double logit = 0.0;
+    for (int i = 0; i < 64; i++) logit = fma(__ldg(P + O::w_head + i), Y[i * MLP_PB + ps], logit);
+    logit += __ldg(P + O::b_head);
+    if (live) a.prob[p] = expit_d(logit);
+  }
 }
 
 // region = dilate(prob >= tau, k) with border clipping; region[g] in {0,1}
