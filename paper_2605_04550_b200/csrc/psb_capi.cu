@@ -86,7 +86,8 @@ struct psb_handle {
   double k_cert_delta = 1e-16;  // PSB_CERT_DELTA=x (0: certificates off, the round-2 overflow rule alone)
   bool k_bexpand = true, k_fallback = true, k_seq = false;
   int k_bvariant = 0;
-  double k_lfrac = 0.5;
+  double k_lfrac = 1.0 / 3.0;
+  int k_defer = 16;
   int k_bfull = 1;
   struct FitEntry { const void* f; int lkey, btpb, tpb, occ, occFull; int64_t threads; int wregs; };
   std::vector<FitEntry> fit_cache;  // engine-B launch shapes per (kernel, engine-L share)
@@ -199,7 +200,8 @@ int psb_create(int device, psb_handle** out) {
   h->k_tau = getenv("PSB_TAU") ? atof(getenv("PSB_TAU")) : 0.0;  // dev: default engine split
   h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 0;  // 0: pick per launch
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
-  h->k_lfrac = getenv("PSB_LFRAC") ? atof(getenv("PSB_LFRAC")) : 0.5;   // dev: SM share hosting an engine-L block (long general lists)
+  h->k_defer = getenv("PSB_DEFER") ? atoi(getenv("PSB_DEFER")) : 16;      // dev: engine-L step deferral (0: off)
+  h->k_lfrac = getenv("PSB_LFRAC") ? atof(getenv("PSB_LFRAC")) : 1.0 / 3.0;   // dev: SM share hosting an engine-L block (long general lists)
   h->k_bfull = getenv("PSB_BFULL") ? atoi(getenv("PSB_BFULL")) : 1;     // dev: 0 restores the two-launch engine B on long general lists
   h->k_refill = getenv("PSB_REFILL") ? atoi(getenv("PSB_REFILL")) : 16;  // dev: engine-L refill threshold
   h->k_cert_delta = getenv("PSB_CERT_DELTA") ? atof(getenv("PSB_CERT_DELTA")) : 1e-16;
@@ -552,14 +554,15 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   // 4.3 ms) because every SM then hosts more engine-L warps next to the FP64-bound bisection warps.
   constexpr int kLWarpsPerBlock = 4;
   const int lsmem = kp.lsmem * kLWarpsPerBlock;
-  // Long general-band lists (C5): engine B is the long pole (FP64-bound, ~1.3 us per point against ~0.2 us for
-  // engine L's, most of which a certificate decides early), and two engine-L blocks leave an SM no room for
-  // a bisection warp. Engine L then takes one block on half of the SMs (1.8x its time with every SM, so it
-  // stays the shorter engine while 3 nB >= nA, i.e. engine B's estimate is twice engine L's), and engine B
-  // is one launch of its full-occupancy grid: its blocks fill the SMs engine L left free at once and the
-  // rest as engine L's blocks retire. Launch shape only: the same bits. C5 matrices 0/4/12/42/10:
-  // 483/522/548/918/645 -> 449/496/527/903/629 ms (a third of the SMs: 442/484/524/900/625, but matrix 4's
-  // engine L then ends 17 ms before engine B; every SM: 471/521/549/920/648).
+  // Long general-band lists (C5): engine B is the long pole (FP64-bound, ~1.3 us per point against ~0.2-0.3 us
+  // for engine L's, most of which a certificate decides early), and two engine-L blocks leave an SM no room
+  // for a bisection warp. Engine L then takes one block on a third of the SMs (it stays the shorter engine
+  // while 3 nB >= nA, i.e. engine B's estimate is at least twice engine L's), and engine B is one launch of
+  // its full-occupancy grid: its blocks fill the SMs engine L left free at once and the rest as engine L's
+  // blocks retire. Launch shape only: the same bits. C5 matrices 0/4/12/42/10, before engine L's step
+  // deferral: two-launch engine B beside engine L on every SM 483/522/548/918/645 ms; one block on every
+  // SM 471/521/549/920/648; on half 449/496/527/903/629; on a third 442/484/524/900/625. With the
+  // deferral (engine L ~25% shorter): half 434/469/516/897/615, a third 428/462/509/891/614.
   const bool long_general = bsw > 0 && nA > 0 && h->k_bfull && !h->k_seq &&
                             nB >= (int64_t)1024 * h->num_sms && 3 * nB >= nA;
   int64_t gridL = 0;
@@ -600,12 +603,13 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     la.scratch = h->scratch.as<double2>(); la.pivs = h->pivs.as<int>();
     la.warp_stride = warp_stride; la.piv_stride = piv_stride;
     la.kmax = kmax; la.refill = std::min(32, std::max(1, opt.refill));
+    la.defer = h->k_defer;
     la.ncert = h->cert;
     la.tcert = std::isfinite(h->cert) ? h->cert * (double)n * (1.0 + 2.0 * kl) : INFINITY;
     la.prof = nullptr;
     if (h->k_prof) {
-      CK(h->prof.ensure(64));
-      CK(cudaMemsetAsync(h->prof.p, 0, 64, st));
+      CK(h->prof.ensure(128));
+      CK(cudaMemsetAsync(h->prof.p, 0, 128, st));
       la.prof = h->prof.as<unsigned long long>();
     }
     CK(cudaEventRecord(h->ev[5], st));
@@ -790,8 +794,10 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   if (ran_fallback) cudaEventElapsedTime(&msF, h->ev[9], h->ev[10]);
   cudaEventElapsedTime(&msT, h->ev[0], ran_fallback ? h->ev[10] : h->ev[4]);
   if (h->k_prof && nA_run > 0) {
-    unsigned long long pr[8];
-    cudaMemcpy(pr, h->prof.p, 64, cudaMemcpyDeviceToHost);
+    unsigned long long pr[16];
+    cudaMemcpy(pr, h->prof.p, 128, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[psb prof] LU lane utilisation %.3f (%llu point-rows of %llu lane-rows the warps' passes ran)\n",
+            pr[9] ? (double)pr[8] / (double)pr[9] : 0.0, pr[8], pr[9]);
     fprintf(stderr, "[psb prof] warp-cycles: lu %.3g s1 %.3g s2 %.3g s3 %.3g s4 %.3g ritz %.3g (gridL %lld) "
             "lane-occupancy of step iterations %.3f over %llu warp-steps\n",
             (double)pr[0], (double)pr[1], (double)pr[2], (double)pr[3], (double)pr[4], (double)pr[5], (long long)gridL,

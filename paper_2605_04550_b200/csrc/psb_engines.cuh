@@ -81,6 +81,7 @@ struct LanArgs {
   int* pivs;                      // per warp: n*32 int32
   int64_t warp_stride, piv_stride;
   int kmax, refill;
+  int defer;                      // step iterations wait for this many factored lanes while points remain (0: never)
   unsigned long long* prof;       // optional: per-phase clock64 totals [lu, s1, s2, s3, s4, ritz, idle]
   // Certificates of singularity to working precision (psb_set_matrix; INFINITY disables them): the point
   // is decided as sigma = 0 (status 2) once sigma_min <= delta ||A e_j||_max <= delta ||A||_2 is proven,
@@ -1020,9 +1021,16 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       int lrows = 0;
       const bool ok = lu_staged<(KL > 0 ? KL : 1), KU>(n, a.Ab, a.LUT, lstage, lane, mine, mine ? z : czero(),
                                                        FU, FL, piv, Tn, Rn, a.tcert, &lrows);
+      const int lrows0 = lrows;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) lrows += __shfl_xor_sync(FULL, lrows, off);
       if (lane == 0) atomicAdd(&a.counters[20], (unsigned long long)lrows);
+      if (a.prof) {  // LU lane utilisation: rows factored for points vs 32 x the rows the warp's pass ran
+        int mx = mine ? lrows0 : 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, off));
+        if (lane == 0) { atomicAdd(&a.prof[8], (unsigned long long)lrows); atomicAdd(&a.prof[9], 32ull * (unsigned long long)mx); }
+      }
       if (mine) {
         if (!ok) {
           finish(0.0, 0, 2);
@@ -1039,6 +1047,12 @@ __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
       if (exhausted && __ballot_sync(FULL, phase != 0) == 0) break;
       continue;
     }
+    // A step iteration costs four sweeps over all n rows whatever the number of lanes stepping. Where the
+    // LU decides most points (C5: ~2% survive it), survivors trickle in at less than one per pass, and
+    // stepping them as they came ran the sweeps at a quarter of the lanes. So while points remain and
+    // fewer than `defer` lanes hold a factored point, those lanes wait and the idle ones take new points
+    // (the refill rule fires: 32 - popc(act) >= refill). Scheduling only: every point's arithmetic is its own.
+    if (!exhausted && __popc(act) < a.defer && 32 - __popc(act) >= a.refill) continue;
     if (a.prof && lane == 0) { atomicAdd(&a.prof[6], (unsigned long long)__popc(act)); atomicAdd(&a.prof[7], 1ull); }
     if (phase == 2 && s1done) {
       s1done = false;

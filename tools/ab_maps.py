@@ -45,7 +45,7 @@ for m in mats:
     eq = np.array_equal(a, b)
     relmax = np.max(np.abs(a - b) / np.maximum(np.abs(a), 1e-300))
     nd = int(np.sum(a != b))
-    dabs = float(np.max(np.abs(a - b))) / float(np.max(a))  # largest change against the map's scale
+    dabs = float(np.max(np.abs(a - b))) / max(float(np.max(a)), 1e-300)  # largest change against the map's scale
     if nd:
         sys.path.insert(0, '.')
         from paper_2605_04550_b200 import configs
