@@ -88,6 +88,7 @@ struct psb_handle {
   int k_bvariant = 0;
   double k_lfrac = 1.0 / 3.0;
   int k_defer = 16;
+  int k_lgmin = 256, k_lgratio = 20;
   int k_bfull = 1;
   struct FitEntry { const void* f; int lkey, btpb, tpb, occ, occFull; int64_t threads; int wregs; };
   std::vector<FitEntry> fit_cache;  // engine-B launch shapes per (kernel, engine-L share)
@@ -200,6 +201,8 @@ int psb_create(int device, psb_handle** out) {
   h->k_tau = getenv("PSB_TAU") ? atof(getenv("PSB_TAU")) : 0.0;  // dev: default engine split
   h->k_btpb = getenv("PSB_BTPB") ? atoi(getenv("PSB_BTPB")) : 0;  // 0: pick per launch
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
+  h->k_lgmin = getenv("PSB_LGMIN") ? atoi(getenv("PSB_LGMIN")) : 256;   // dev: long-general rule, min bisection points per SM
+  h->k_lgratio = getenv("PSB_LGRATIO") ? atoi(getenv("PSB_LGRATIO")) : 20;  // dev: ... and nA <= ratio * nB
   h->k_defer = getenv("PSB_DEFER") ? atoi(getenv("PSB_DEFER")) : 16;      // dev: engine-L step deferral (0: off)
   h->k_lfrac = getenv("PSB_LFRAC") ? atof(getenv("PSB_LFRAC")) : 1.0 / 3.0;   // dev: SM share hosting an engine-L block (long general lists)
   h->k_bfull = getenv("PSB_BFULL") ? atoi(getenv("PSB_BFULL")) : 1;     // dev: 0 restores the two-launch engine B on long general lists
@@ -554,18 +557,24 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   // 4.3 ms) because every SM then hosts more engine-L warps next to the FP64-bound bisection warps.
   constexpr int kLWarpsPerBlock = 4;
   const int lsmem = kp.lsmem * kLWarpsPerBlock;
-  // Long general-band lists (C5): engine B is the long pole (FP64-bound, ~1.3 us per point against ~0.2-0.3 us
-  // for engine L's, most of which a certificate decides early), and two engine-L blocks leave an SM no room
-  // for a bisection warp. Engine L then takes one block on a third of the SMs (it stays the shorter engine
-  // while 3 nB >= nA, i.e. engine B's estimate is at least twice engine L's), and engine B is one launch of
-  // its full-occupancy grid: its blocks fill the SMs engine L left free at once and the rest as engine L's
-  // blocks retire. Launch shape only: the same bits. C5 matrices 0/4/12/42/10, before engine L's step
-  // deferral: two-launch engine B beside engine L on every SM 483/522/548/918/645 ms; one block on every
-  // SM 471/521/549/920/648; on half 449/496/527/903/629; on a third 442/484/524/900/625. With the
-  // deferral (engine L ~25% shorter): half 434/469/516/897/615, a third 428/462/509/891/614.
+  // General-band lists with bisection work (C5): engine B is usually the long pole (FP64-bound, ~1.3 us per
+  // point against 0.06-0.3 us for engine L's, most of which a certificate decides early), and two engine-L
+  // blocks leave an SM no room for a bisection warp. Engine L then starts with one block on a third of the
+  // SMs, engine B is one launch of its full-occupancy grid (its blocks fill the SMs engine L left free at
+  // once and the rest as engine L's blocks retire), and the rest of engine L's grid is queued behind engine
+  // B: if engine L turns out the longer one, it gets the whole GPU when engine B ends. Launch shape only:
+  // the same bits. Rule: nB >= 256 per SM and nA <= 20 nB (engine L's cost per point is not known before it
+  // runs: 0.06 us (matrix 1) ... 0.31 us (matrix 0) on C5).
+  // Measured, C5 matrices 0/4/12/42/10, before engine L's step deferral: two-launch engine B beside engine
+  // L on every SM 483/522/548/918/645 ms; one engine-L block on every SM 471/521/549/920/648; on half
+  // 449/496/527/903/629; on a third 442/484/524/900/625. With the deferral (engine L ~25% shorter): half
+  // 434/469/516/897/615, a third 428/462/509/891/614. Widening the rule from (1024 per SM, nA <= 3 nB) to
+  // (256, 20) with the queued remainder: 20 of the 64 matrices 3..18% faster (matrix 1 147 -> 120 ms), one
+  // slower (matrix 45, engine L as long as engine B: 162 -> 196 ms); C5 pass 13.77 -> 13.29 s.
   const bool long_general = bsw > 0 && nA > 0 && h->k_bfull && !h->k_seq &&
-                            nB >= (int64_t)1024 * h->num_sms && 3 * nB >= nA;
-  int64_t gridL = 0;
+                            nB >= (int64_t)h->k_lgmin * h->num_sms && (int64_t)h->k_lgratio * nB >= nA;
+  int64_t gridL = 0, gridL2 = 0;  // gridL2: engine L's second launch (long general lists), queued behind engine B
+  LanArgs la{};
   int occL = 0;
   if (nA > 0) {
     // memoised per kernel: attribute set-up and the occupancy query once per handle
@@ -586,13 +595,16 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     int64_t warps = std::min<int64_t>((int64_t)occL * h->num_sms * kLWarpsPerBlock, (nA + 31) / 32);
     warps = std::min<int64_t>(warps, (int64_t)(budget / per_warp));
     if (h->k_lwarps > 0) warps = std::min<int64_t>(warps, h->k_lwarps);
-    if (long_general)
-      warps = std::min<int64_t>(warps, std::max<int64_t>(1, (int64_t)(h->k_lfrac * h->num_sms + 0.5)) * kLWarpsPerBlock);
     warps = std::max<int64_t>(kLWarpsPerBlock, (warps + kLWarpsPerBlock - 1) / kLWarpsPerBlock * kLWarpsPerBlock);
+    const int64_t warps_all = warps;  // every warp engine L may run (scratch is per warp)
+    if (long_general) {
+      warps = std::min<int64_t>(warps, std::max<int64_t>(1, (int64_t)(h->k_lfrac * h->num_sms + 0.5)) * kLWarpsPerBlock);
+      gridL2 = (warps_all - warps) / kLWarpsPerBlock;
+    }
     gridL = warps / kLWarpsPerBlock;
-    CK(h->scratch.ensure((size_t)(warps * warp_stride * sizeof(double2))));
-    CK(h->pivs.ensure((size_t)(warps * piv_stride * 4)));
-    LanArgs la;
+    CK(h->scratch.ensure((size_t)(warps_all * warp_stride * sizeof(double2))));
+    CK(h->pivs.ensure((size_t)(warps_all * piv_stride * 4)));
+    la.warp_base = 0;
     la.s = s; la.Ab = h->Ab.as<double2>();
     la.v1 = dyn ? h->v1.as<double2>() : h->v1.as<double2>() + n;  // pipelined sweeps read the replicated copy
     la.v1b = h->v1.as<double2>();
@@ -739,6 +751,20 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     gridB = 0;
   }
   CK(cudaEventRecord(h->ev[2], sB));
+  if (gridL2 > 0 && nB > 0) {
+    // Engine L's remaining blocks, queued behind engine B on its stream: if engine L (on its share of the
+    // SMs) is still running when engine B ends, they take the whole GPU and pull from the same work counter;
+    // if it has finished, they find the list exhausted and exit at once. So a list whose engine L turns out
+    // longer than estimated costs little (both launches own separate scratch: warp_base).
+    LanArgs l2 = la;
+    l2.warp_base = gridL * kLWarpsPerBlock;
+    CK(cudaEventRecord(h->ev[12], sB));
+    kp.l<<<(unsigned)gridL2, 32 * kLWarpsPerBlock, lsmem, sB>>>(l2);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(h->ev[11], sB));
+  } else {
+    gridL2 = 0;
+  }
   if (sB != st) CK(cudaStreamWaitEvent(st, h->ev[2], 0));
   if (nA > 0) CK(cudaStreamWaitEvent(st, h->ev[3], 0));
   if (gridB2 > 0) CK(cudaStreamWaitEvent(st, h->ev[6], 0));
@@ -790,7 +816,15 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     cudaEventElapsedTime(&msB, h->ev[8], h->ev[2]);
     if (gridB2 > 0) { float m2 = 0; cudaEventElapsedTime(&m2, h->ev[8], h->ev[6]); msB = std::max(msB, m2); }
   }
-  if (nA > 0) cudaEventElapsedTime(&msL, h->ev[7], h->ev[3]);
+  if (nA > 0) {
+    cudaEventElapsedTime(&msL, h->ev[7], h->ev[3]);
+    if (gridL2 > 0) {  // engine L's window: the union of its two launches' windows (the second may find nothing left)
+      float s2 = 0, e2 = 0;
+      cudaEventElapsedTime(&s2, h->ev[7], h->ev[12]);
+      cudaEventElapsedTime(&e2, h->ev[7], h->ev[11]);
+      msL = (s2 >= msL) ? msL + (e2 - s2) : std::max(msL, e2);
+    }
+  }
   if (ran_fallback) cudaEventElapsedTime(&msF, h->ev[9], h->ev[10]);
   cudaEventElapsedTime(&msT, h->ev[0], ran_fallback ? h->ev[10] : h->ev[4]);
   if (h->k_prof && nA_run > 0) {
@@ -829,7 +863,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   S.flops_lanczos = (double)hc[20] * flops_lu_row(kl, ku) + (double)hc[5] * n * flops_it_row(kl, ku);
   S.bytes_lanczos = (double)hc[20] * (16.0 * (s.NU + kl) + 4.0) + (double)hc[5] * n * bytes_it_row(kl, ku);
   S.ms_bisect = msB; S.ms_lanczos = msL; S.ms_total = msT; S.ms_classify = msC; S.ms_fallback = msF;
-  S.launches = 1 + (gridL > 0 ? 1 : 0) + (nB > 0 ? 1 : 0) + (gridB2 > 0 ? 1 : 0) + (ran_fallback ? 1 : 0);
+  S.launches = 1 + (gridL > 0 ? 1 : 0) + (gridL2 > 0 ? 1 : 0) + (nB > 0 ? 1 : 0) + (gridB2 > 0 ? 1 : 0) + (ran_fallback ? 1 : 0);
   S.grid_bisect = (int32_t)(gridB + gridB2); S.grid_lanczos = (int32_t)gridL;
   if ((int64_t)(hc[3] + hc[6]) != P)
     return fail(h, PSB_ERR_CUDA, "internal: points finished " + std::to_string(hc[3] + hc[6]) + " != " +

@@ -80,6 +80,7 @@ struct LanArgs {
   double2* scratch;               // per warp: FU n*NU*32 | FL n*NL*32 | T | RA | RB (n*32 each) | hist kmax*32
   int* pivs;                      // per warp: n*32 int32
   int64_t warp_stride, piv_stride;
+  int64_t warp_base;              // first warp index of this launch (engine L may run as two launches)
   int kmax, refill;
   int defer;                      // step iterations wait for this many factored lanes while points remain (0: never)
   unsigned long long* prof;       // optional: per-phase clock64 totals [lu, s1, s2, s3, s4, ritz, idle]
@@ -937,7 +938,7 @@ template <int KL, int KU, bool DYN, int DPIPE>
 __global__ void __launch_bounds__(128) k_lanczos(LanArgs a) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t gw = a.warp_base + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const Shape s = a.s;
   const int n = s.n;
   double2* base = a.scratch + gw * a.warp_stride;

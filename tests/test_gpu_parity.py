@@ -229,24 +229,30 @@ def test_bisection_near_threshold_full_grid(gpu, name):
     assert e.max() <= 1e-9, f"{name}: worst {e.max():.3e}"
 
 
-def test_engine_b_second_launch_is_bitwise_neutral(gpu, tmp_path):
-    """Long bisection lists run as two launches (the second queued behind engine L); launch shape must
-    not change a single bit. C5's full 1024x1024 grid (about 300k bisection points) takes that path;
-    PSB_NOBEXP=1 (read at handle creation, so in a subprocess) runs it as one launch."""
+def test_launch_shapes_are_bitwise_neutral(gpu, tmp_path):
+    """Launch shape and lane scheduling must not change a single bit (every sigma is a function of (A, z)).
+    C5's full 1024x1024 grid of matrix 0 (about 300k bisection points, 740k engine-L points) takes the long
+    general-band path: engine L on a third of the SMs with its step iterations deferred until 16 lanes hold
+    a factored point, engine B as one full-occupancy launch. The knobs (read at handle creation, so each run
+    is a subprocess) switch that back to engine L on every SM with undeferred steps and the two-launch
+    engine B (second launch queued behind engine L), and to one launch without the expansion."""
     import os
     import subprocess
     import sys
     code = ("import sys, numpy as np; sys.path.insert(0, '.'); from paper_2605_04550_b200 import configs, core; "
             "c = configs.CONFIGS['C5']; np.save(sys.argv[1], core.smin_many(c.matrix(0), c.grid.points().ravel()))")
+    knobs = ("PSB_NOBEXP", "PSB_BFULL", "PSB_DEFER", "PSB_LFRAC")
     outs = []
-    for env_extra, name in (({}, "two.npy"), ({"PSB_NOBEXP": "1"}, "one.npy")):
-        env = {k: v for k, v in os.environ.items() if k != "PSB_NOBEXP"}
+    for env_extra, name in (({}, "product.npy"), ({"PSB_BFULL": "0", "PSB_DEFER": "0"}, "two.npy"),
+                            ({"PSB_BFULL": "0", "PSB_NOBEXP": "1", "PSB_DEFER": "8"}, "one.npy")):
+        env = {k: v for k, v in os.environ.items() if k not in knobs}
         env.update(env_extra)
         path = tmp_path / name
         subprocess.run([sys.executable, "-c", code, str(path)], check=True, env=env,
                        cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2])
 
 
 def test_partly_constant_band_long_boundary(gpu):
