@@ -255,6 +255,41 @@ def test_launch_shapes_are_bitwise_neutral(gpu, tmp_path):
     assert np.array_equal(outs[0], outs[2])
 
 
+def test_general_band_long_list_shapes_and_parity(gpu, tmp_path):
+    """A mid-size noisy (2,2) band (general-band kernels, runtime knobs as above) on a 400x400 grid: enough
+    bisection points for the long-list launch shape (engine L on a third of the SMs plus its queued second
+    launch, engine B as one launch, step deferral). The map must equal the one computed with those shapes
+    switched off, bit for bit, and a seeded sample of it must match zgesdd."""
+    import os
+    import subprocess
+    import sys
+    from oracle.sigma_oracle import smin_restated
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); from paper_2605_04550_b200 import core\n"
+        "rng = np.random.default_rng(5); n = 300\n"
+        "c = rng.standard_normal(5) + 1j * rng.standard_normal(5)\n"
+        "A = sum(np.diag(np.full(n - abs(d), c[d + 2]) + 1e-3 * (rng.standard_normal(n - abs(d)) + 1j * "
+        "rng.standard_normal(n - abs(d))), d) for d in range(-2, 3))\n"
+        "r = np.abs(c).sum(); g = core.make_grid(-1.2 * r, 1.2 * r, -1.2 * r, 1.2 * r, 400, 400)\n"
+        "f = core.full_pseudospectrum(A, g); st = core.last_stats()\n"
+        "np.savez(sys.argv[1], A=A, zs=g.points().ravel(), v=f.values.ravel(), nb=st['n_bisect'], nl=st['n_lanczos'])\n")
+    knobs = ("PSB_NOBEXP", "PSB_BFULL", "PSB_DEFER", "PSB_LFRAC")
+    outs = []
+    for env_extra, name in (({}, "product.npz"), ({"PSB_BFULL": "0", "PSB_DEFER": "0"}, "plain.npz")):
+        env = {k: v for k, v in os.environ.items() if k not in knobs}
+        env.update(env_extra)
+        path = tmp_path / name
+        subprocess.run([sys.executable, "-c", code, str(path)], check=True, env=env,
+                       cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+        outs.append(np.load(path))
+    a, b = outs
+    assert int(a["nb"]) >= 256 * 148 and int(a["nl"]) > 0, (int(a["nb"]), int(a["nl"]))
+    assert np.array_equal(a["v"], b["v"])
+    idx = np.random.default_rng(9).choice(a["v"].size, 48, replace=False)
+    worst = check(a["v"][idx], smin_restated(a["A"], a["zs"][idx]), np.linalg.norm(a["A"], 2), "general long list")
+    print(f"[general long list] nB {int(a['nb'])}, nL {int(a['nl'])}, worst floored rel err {worst:.2e}")
+
+
 def test_partly_constant_band_long_boundary(gpu):
     """A band that is diagonal-constant only over its second half: the constant interior is long
     enough to detect but its boundary (60 rows) exceeds the per-thread slot budget, so the general
