@@ -619,6 +619,8 @@ struct LogDet {
 #endif
   }
   PSB_HD double value() const { return log(mant) + 0.6931471805599453 * expo; }
+  // log |det| (a failed probe's product carries the sign of its negative pivots)
+  PSB_HD double absvalue() const { return log(fabs(mant)) + 0.6931471805599453 * expo; }
 };
 
 // Same as pdw_load_row with the G row entries given (rows of a diagonal-constant band share them).
@@ -636,14 +638,19 @@ PSB_HD void pdw_load_row_g(PDWin<KLM, KUM> (&Wn)[NP], int r, const double2 (&g)[
   }
 }
 
+// pos[q] counts the positive pivots of probe q: after all n rows, n - pos is the number of negative pivots,
+// i.e. (Sylvester) the number of sigma_i^2 below the probe - a hint for placing the next probes of a failed
+// round (k_bisect), never a decision: the PD answers alone move the bracket.
 template <int KLM, int KUM, int NP, bool LD = true>
-PSB_HD void pdw_step(PDWin<KLM, KUM> (&Wn)[NP], bool (&pd)[NP], LogDet (&ld)[NP]) {
+PSB_HD void pdw_step(PDWin<KLM, KUM> (&Wn)[NP], bool (&pd)[NP], LogDet (&ld)[NP], int (&pos)[NP]) {
   constexpr int B = KLM + KUM;
 #pragma unroll
   for (int q = 0; q < NP; q++) {
     auto& W = Wn[q].W;
     const double dj = W[0][0].x;
-    pd[q] = pd[q] && (dj > 0.0);
+    const bool positive = dj > 0.0;
+    pd[q] = pd[q] && positive;
+    pos[q] += positive ? 1 : 0;
     if (LD) ld[q].mant *= dj;
     const double iD = fast_rcp(dj);
     double2 l[B + 1];
@@ -678,8 +685,11 @@ PSB_HD void pdw_test(int n, const double2* __restrict__ Ab, double2 z,
   for (int q = 0; q < NP; q++) ld[q].init();
 #pragma unroll
   for (int r = 0; r <= B; r++) pdw_load_row<KLM, KUM, NP>(Wn, r, n, r, Ab, z, zz);
+  int pos[NP];
+#pragma unroll
+  for (int q = 0; q < NP; q++) pos[q] = 0;
   for (int j = 0; j < n; j++) {
-    pdw_step<KLM, KUM, NP>(Wn, pd, ld);
+    pdw_step<KLM, KUM, NP>(Wn, pd, ld, pos);
     pdw_load_row<KLM, KUM, NP>(Wn, B, n, j + 1 + B, Ab, z, zz);
     if ((j & 15) == 15)
       for (int q = 0; q < NP; q++) ld[q].norm();

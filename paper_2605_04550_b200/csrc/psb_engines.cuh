@@ -34,6 +34,9 @@ struct BisArgs {
   int fallback;                   // 1: listB holds engine-L points that did not converge (forced, [0, lambda_tau]);
   double rmin2;                   //    their result is kept only where sigma^2 >= rmin2 X(z)^2 (squared form accurate)
   int secant;                     // 1: secant-accelerated multisection (G == 1, NP == 2 shapes)
+  int counts;                     // 1: count-guided probe placement (negative-pivot counts of failed probes)
+  int cnt_min;                    //    least count of the lower failure
+  double cnt_slack;               //    probes at the estimate -/+ (hi - estimate) * cnt_slack / count
   int tz_j0, tz_j1;               // rows [tz_j0, tz_j1] share one G row (diagonal-constant band); j0 > j1: none
   double2* gb;                    // TZ kernels: per-thread G rows formed once per point, lane-interleaved
                                   //   (stride gb_T threads): slots [0, nb) the boundary rows, slot nb the interior row
@@ -395,6 +398,13 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   // secant acceleration state (G == 1): log det at lo and at the previous PD point lp
   double Llo = 0.0, lp = 0.0, Lp = 0.0;
   bool have_lo = false, have_p = false, use_sec = false;
+  // the two lowest failed probes that carry a negative-pivot count (fa < fb; counts ca <= cb)
+  double fa = INFINITY, fb = INFINITY;
+  int ca = 0, cb = 0;
+  bool use_cnt = true;
+  // log |det| at hi when exactly one sigma_i^2 lies below it (the root is isolated: det changes sign once)
+  double Lhi = 0.0, ifrac = 0.0625;
+  bool have_hi = false, use_itp = true;
   bool exhausted = false;
   const int64_t total = (a.mode == 0) ? a.P : (int64_t)a.counters[7];
   while (true) {
@@ -457,6 +467,8 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
               if (u2 > lo) hi = u2;
             }
             have_lo = have_p = use_sec = false;
+            fa = fb = INFINITY; ca = cb = 0; use_cnt = true;
+            have_hi = false; use_itp = true; ifrac = 0.0625;
             if (a.mode == 1 && forced) { lo = 0.0; hi = lam_tau; phase = 2; }
           }
         }
@@ -497,9 +509,67 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         }
       }
     }
+    // Count-guided step: a failed probe's LDL^H has as many negative pivots as there are sigma_i^2 below it.
+    // Near the bottom edge of a banded spectrum the count grows like N(lambda)^2 ~ (lambda - sigma_1^2) / kappa
+    // (sigma_k^2 ~ sigma_1^2 + kappa (k^2 - 1)), so the two lowest counted failures (fa, ca), (fb, cb) give
+    // the estimate s = (fa - r fb) / (1 - r), r = ((ca + 1/2)^2 - 1) / ((cb + 1/2)^2 - 1). While the bracket
+    // still holds several singular values (ca >= cnt_min = 2) a three-section round buys 1.58 bits, the
+    // estimate several; the round probes s -/+ the estimate's slack (hi - s) cnt_slack / ca. Measured (B200,
+    // tests per bisection point / kernel ms): C5 matrix 0 41.3 / 425 without, 35.6 / 381 with (cnt_min 2,
+    // slack 2; cnt_min 3: 36.1 / 384, 6: 37.6 / 397; slack 1: 35.1 / 382, 4: 37.4 / 394); C3 41.8 / 14.4 ->
+    // 36.5 / 13.5. Using the counts during the search phase as well changed nothing. Only the PD answers move the bracket, so a poor
+    // estimate costs a round, never correctness; a round that did not shrink the bracket 3x falls back.
+    bool cnt_round = false;
+    if constexpr (SEC) {
+      if (a.counts && a.mode == 1 && me && phase == 2 && use_cnt && ca >= a.cnt_min && cb > ca && fa == hi && fb > fa) {
+        const double wa = ((double)ca + 0.5) * ((double)ca + 0.5) - 1.0;
+        const double wb = ((double)cb + 0.5) * ((double)cb + 0.5) - 1.0;
+        const double r = wa / wb;
+        const double s = (fa - r * fb) / (1.0 - r);
+        if (s > lo && s < hi) {
+          const double slack = (hi - s) * fmax(a.cnt_slack / (double)ca, 0.02);
+          double p0 = s - slack, p1 = s + slack;
+          if (!(p0 > lo)) p0 = lo + 0.25 * (s - lo);
+          if (!(p1 < hi)) p1 = 0.5 * (s + hi);
+          if (p0 > lo && p0 < p1 && p1 < hi) {
+#pragma unroll
+            for (int q = 0; q < NP; q++) lam[q] = (gl * NP + q == 0) ? p0 : p1;
+            cnt_round = true;
+          }
+        }
+      }
+    }
+    // Isolated root: once the failed end of the bracket has exactly one negative pivot, det G changes sign
+    // exactly once inside [lo, hi] and is nearly linear there (the other factors sigma_i^2 - lambda barely
+    // move over a bracket narrower than the spacing), so the chord between det(lo) > 0 and det(hi) < 0
+    // (from the two log |det|) lands on sigma_1^2 to second order. The round probes the chord's root -/+
+    // ifrac of the bracket; ifrac squares after every round that caught the root between its probes.
+    bool itp_round = false;
+    if constexpr (SEC) {
+      if (a.counts && a.mode == 1 && me && phase == 2 && use_itp && have_lo && have_hi && hi < INFINITY) {
+        const double t = 1.0 / (1.0 + exp(Lhi - Llo));  // det(lo) / (det(lo) - det(hi))
+        const double w = hi - lo;
+        const double s = lo + w * t;
+        if (s > lo && s < hi) {
+          const double dlt = w * ifrac;
+          double p0 = s - dlt, p1 = s + dlt;
+          if (!(p0 > lo)) p0 = lo + 0.5 * (s - lo);
+          if (!(p1 < hi)) p1 = s + 0.5 * (hi - s);
+          if (p0 > lo && p0 < p1 && p1 < hi) {
+#pragma unroll
+            for (int q = 0; q < NP; q++) lam[q] = (gl * NP + q == 0) ? p0 : p1;
+            itp_round = true;
+            cnt_round = false;
+          }
+        }
+      }
+    }
     const double2 zt = me ? z : czero();
     bool pd[NP];
     LogDet ld[NP];
+    int pos[NP];
+#pragma unroll
+    for (int q = 0; q < NP; q++) pos[q] = 0;
     int rows = a.n;  // LDL^H rows this warp executed in this round (tests stop early once every probe failed)
 #pragma unroll
     for (int q = 0; q < NP; q++) { pd[q] = true; ld[q].init(); }
@@ -557,6 +627,10 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       bool stop = false;
       rows = 0;
       auto vote = [&]() {
+        // (Not in the multisection with counts: a failed probe's count needs every row, and whether a warp
+        // could stop depends on its other lanes - a point's probe sequence must depend on (A, z) alone.
+        // There the vote rarely fired anyway: it takes every probe of all 32 lanes failing.)
+        if (a.mode == 1 && a.counts) return;
         bool any = false;
 #pragma unroll
         for (int q = 0; q < NP; q++) any = any || pd[q];
@@ -574,14 +648,14 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         for (; !stop && j + 8 <= j1; j += 8) {
 #pragma unroll
           for (int u = 0; u < 8; u++) {
-            pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+            pdw_step<KL, KU, NP, SEC>(Wn, pd, ld, pos);
             loader(j + u + 1 + B);
           }
           norm();
           if (((j - j0) & 31) == 24) vote();
         }
         for (; !stop && j < j1; j++) {
-          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld, pos);
           loader(j + 1 + B);
           if (((j - j0) & 7) == 7) norm();
         }
@@ -591,7 +665,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
       // short edge segments: a plain row loop (keeps the unrolled code, and registers, to one body)
       auto run1 = [&](int j0, int j1) {
         for (int j = j0; j < j1; j++) {
-          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld, pos);
           gslot(B, j + 1 + B);
           if (((j - j0) & 7) == 7) norm();
         }
@@ -656,7 +730,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
           const double2* st = stg + sidx * BR::SE;
 #pragma unroll
           for (int u = 0; u < 8; u++) {
-            pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+            pdw_step<KL, KU, NP, SEC>(Wn, pd, ld, pos);
             load_staged(st + u * BR::RW, j + u + 1 + B);
           }
           norm();
@@ -667,7 +741,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         cp_wait<0>();
         __syncwarp();
         for (; !stop && j < a.n; j++) {
-          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld);
+          pdw_step<KL, KU, NP, SEC>(Wn, pd, ld, pos);
           pdw_load_row<KL, KU, NP, true>(Wn, B, a.n, j + 1 + B, a.Ab, zt, zz, a.AHA);
           if ((j & 7) == 7) norm();
         }
@@ -711,17 +785,26 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
     // the group's probes in ascending order i = gl * NP + q, with the log dets of the PD ones
     double lamK[K], LK[K];
     bool pdK[K];
+    int cK[K];  // negative pivots of the failed probes whose test ran every row (0: no count)
     if constexpr (SEC) {
+      const bool full = rows == a.n;
       if constexpr (G == 1) {
 #pragma unroll
-        for (int q = 0; q < NP; q++) { lamK[q] = lam[q]; pdK[q] = pd[q]; LK[q] = pd[q] ? ld[q].value() : 0.0; }
+        for (int q = 0; q < NP; q++) {
+          lamK[q] = lam[q]; pdK[q] = pd[q];
+          cK[q] = (!pd[q] && full) ? a.n - pos[q] : 0;
+          LK[q] = pd[q] ? ld[q].value() : (cK[q] == 1 ? ld[q].absvalue() : 0.0);
+        }
       } else {  // G == 2, NP == 1: probe 0 on the group's even lane, probe 1 on the odd one
-        const double myL = pd[0] ? ld[0].value() : 0.0;
+        const int myc = (!pd[0] && full) ? a.n - pos[0] : 0;
+        const double myL = pd[0] ? ld[0].value() : (myc == 1 ? ld[0].absvalue() : 0.0);
         const double oL = __shfl_xor_sync(FULL, myL, 1, 2), olam = __shfl_xor_sync(FULL, lam[0], 1, 2);
         const bool opd = __shfl_xor_sync(FULL, (int)pd[0], 1, 2) != 0;
+        const int oc = __shfl_xor_sync(FULL, myc, 1, 2);
         lamK[0] = gl == 0 ? lam[0] : olam; lamK[1] = gl == 0 ? olam : lam[0];
         pdK[0] = gl == 0 ? pd[0] : opd;    pdK[1] = gl == 0 ? opd : pd[0];
         LK[0] = gl == 0 ? myL : oL;        LK[1] = gl == 0 ? oL : myL;
+        cK[0] = gl == 0 ? myc : oc;        cK[1] = gl == 0 ? oc : myc;
       }
     }
     if (me) {
@@ -741,6 +824,29 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         lo = fmax(lo, nlo);
         const double new_w = nhi - lo;
         use_sec = (phase == 2 || phi < INFINITY) && !(new_w > old_w / 3.0);  // keep going while it pays
+        // counted failures: keep the two lowest; a count-guided round that did not pay sits out one round
+#pragma unroll
+        for (int q = 0; q < K; q++) {
+          if (!pdK[q] && cK[q] > 0) {
+            if (lamK[q] < fa) { fb = fa; cb = ca; fa = lamK[q]; ca = cK[q]; }
+            else if (lamK[q] > fa && lamK[q] < fb) { fb = lamK[q]; cb = cK[q]; }
+          }
+        }
+        use_cnt = cnt_round ? !(new_w > old_w / 3.0) : true;
+        // the failed end: if it moved, it carries a usable log |det| only when its count is exactly one
+        if (nhi < hi) {
+          have_hi = false;
+#pragma unroll
+          for (int q = 0; q < K; q++)
+            if (!pdK[q] && lamK[q] == nhi && cK[q] == 1 && isfinite(LK[q])) { have_hi = true; Lhi = LK[q]; }
+        }
+        if (itp_round) {
+          const bool caught = !(new_w > 2.5 * ifrac * old_w);
+          use_itp = !(new_w > old_w / 3.0);
+          ifrac = caught ? fmax(ifrac * ifrac, 1e-7) : 0.0625;
+        } else {
+          use_itp = true;
+        }
       }
       if (phase == 1 && nlo < nhi) {
         // search: upward by 4x/16x while no upper bound, else geometric; the linear multisection /
