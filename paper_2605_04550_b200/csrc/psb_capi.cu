@@ -478,12 +478,12 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   h->stats.n_points = P;
   if (P == 0) return PSB_OK;
 
-  CK(h->counters.ensure(sizeof(unsigned long long) * 24));  // [16..19]: row counters (classify, B, fallback, B2), [20] LU rows
+  CK(h->counters.ensure(sizeof(unsigned long long) * 48));  // [16..19]: row counters (classify, B, fallback, B2), [20] LU rows
   CK(h->listA.ensure(sizeof(int64_t) * P));
   CK(h->listB.ensure(sizeof(int64_t) * P));
   CK(h->listF.ensure(sizeof(int64_t) * P));
   unsigned long long* cnt = h->counters.as<unsigned long long>();
-  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 24, st));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 48, st));
 
   // ---- classification: one LDL^H test per point at lambda = (tau S)^2 splits the points
   // general-band static kernels stage their G-row coefficients per warp in dynamic shared memory
@@ -509,6 +509,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   ba.counts = h->k_counts;
   ba.cnt_min = 2;
   ba.cnt_slack = 2.0;
+  ba.itp_frac0 = 0.0625;
   ba.tz_j0 = h->k_toeplitz ? h->tz_j0 : 1;
   ba.tz_j1 = h->k_toeplitz ? h->tz_j1 : 0;
   const int64_t gridC = std::max<int64_t>(1, std::min<int64_t>((int64_t)occB * h->num_sms, (P + 127) / 128));
@@ -774,7 +775,7 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   if (nA > 0) CK(cudaStreamWaitEvent(st, h->ev[3], 0));
   if (gridB2 > 0) CK(cudaStreamWaitEvent(st, h->ev[6], 0));
   CK(cudaEventRecord(h->ev[4], st));
-  unsigned long long hc[24];
+  unsigned long long hc[32];
   CK(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   bool ran_fallback = false;
@@ -811,6 +812,9 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     ran_fallback = true;
   }
   const int64_t nA_run = (int64_t)hc[1], nB_run = (int64_t)hc[7];
+  if (getenv("PSB_ROUND_STATS") && hc[3] > 0)
+    fprintf(stderr, "[psb rounds] per bisection point: search %.2f section %.2f secant %.2f count %.2f chord %.2f\n",
+            (double)hc[24] / hc[3], (double)hc[25] / hc[3], (double)hc[26] / hc[3], (double)hc[27] / hc[3], (double)hc[28] / hc[3]);
   // Per-launch windows from events recorded on each kernel's own stream right before and after it, with
   // no host round trip inside any window (roofline denominators, bench.py):
   //   classification ev0 -> ev1; engine L ev7 -> ev3 (stream2); engine B ev8 -> the later of its own end

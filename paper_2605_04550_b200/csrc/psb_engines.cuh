@@ -37,6 +37,7 @@ struct BisArgs {
   int counts;                     // 1: count-guided probe placement (negative-pivot counts of failed probes)
   int cnt_min;                    //    least count of the lower failure
   double cnt_slack;               //    probes at the estimate -/+ (hi - estimate) * cnt_slack / count
+  double itp_frac0;               //    chord step: first half-width as a fraction of the bracket
   int tz_j0, tz_j1;               // rows [tz_j0, tz_j1] share one G row (diagonal-constant band); j0 > j1: none
   double2* gb;                    // TZ kernels: per-thread G rows formed once per point, lane-interleaved
                                   //   (stride gb_T threads): slots [0, nb) the boundary rows, slot nb the interior row
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
   int ca = 0, cb = 0;
   bool use_cnt = true;
   // log |det| at hi when exactly one sigma_i^2 lies below it (the root is isolated: det changes sign once)
-  double Lhi = 0.0, ifrac = 0.0625;
+  double Lhi = 0.0, ifrac = a.itp_frac0;
   bool have_hi = false, use_itp = true;
   bool exhausted = false;
   const int64_t total = (a.mode == 0) ? a.P : (int64_t)a.counters[7];
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
             }
             have_lo = have_p = use_sec = false;
             fa = fb = INFINITY; ca = cb = 0; use_cnt = true;
-            have_hi = false; use_itp = true; ifrac = 0.0625;
+            have_hi = false; use_itp = true; ifrac = a.itp_frac0;
             if (a.mode == 1 && forced) { lo = 0.0; hi = lam_tau; phase = 2; }
           }
         }
@@ -495,6 +496,9 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
     // and convex below sigma_min^2, so the secant through two PD points (lp, lo) has its root ls below
     // sigma_min^2 (a valid lower bound). Probe ls and ls + (ls - lo)/10; the PD tests alone decide
     // the bracket, so a poor secant costs time, never correctness.
+#ifdef PSB_ROUND_STATS
+    int rtype = (phase == 1) ? 0 : 1;  // 0 search, 1 section, 2 secant, 3 count, 4 chord
+#endif
     if constexpr (SEC) {
       if (a.mode == 1 && me && phase == 2 && use_sec && have_lo && have_p && a.secant) {
         const double dL = Lp - Llo;  // log(f(lp) / f(lo)) > 0 (NaN if a product overflowed)
@@ -505,6 +509,9 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
             if (!(p1 < hi)) p1 = 0.5 * (ls + hi);
 #pragma unroll
             for (int q = 0; q < NP; q++) lam[q] = (gl * NP + q == 0) ? ls : p1;  // probe 0: ls, probe 1: p1
+#ifdef PSB_ROUND_STATS
+            rtype = 2;
+#endif
           }
         }
       }
@@ -535,6 +542,9 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
 #pragma unroll
             for (int q = 0; q < NP; q++) lam[q] = (gl * NP + q == 0) ? p0 : p1;
             cnt_round = true;
+#ifdef PSB_ROUND_STATS
+            rtype = 3;
+#endif
           }
         }
       }
@@ -543,7 +553,12 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
     // exactly once inside [lo, hi] and is nearly linear there (the other factors sigma_i^2 - lambda barely
     // move over a bracket narrower than the spacing), so the chord between det(lo) > 0 and det(hi) < 0
     // (from the two log |det|) lands on sigma_1^2 to second order. The round probes the chord's root -/+
-    // ifrac of the bracket; ifrac squares after every round that caught the root between its probes.
+    // ifrac of the bracket; ifrac goes to its power 3/2 after every round that caught the root between its
+    // probes and back to 1/16 after a miss. Measured (C5 matrix 0, tests per bisection point / kernel ms):
+    // without counts and chord 41.3 / 425; counts only 35.6 / 381; with the chord, first half-width 1/16:
+    // power 2 32.3 / 316, power 3/2 31.5 / 309, power 3 35.7 / 349; first half-width 1/4, 1/8, 1/32 (power
+    // 2): 318, 323, 351 ms. Probing the PD secant's root and the chord's root (a lower and an upper bound
+    // while det is convex) instead of root -/+ ifrac took more rounds (6.6 against 6.1 chord rounds).
     bool itp_round = false;
     if constexpr (SEC) {
       if (a.counts && a.mode == 1 && me && phase == 2 && use_itp && have_lo && have_hi && hi < INFINITY) {
@@ -560,6 +575,9 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
             for (int q = 0; q < NP; q++) lam[q] = (gl * NP + q == 0) ? p0 : p1;
             itp_round = true;
             cnt_round = false;
+#ifdef PSB_ROUND_STATS
+            rtype = 4;
+#endif
           }
         }
       }
@@ -807,6 +825,9 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         cK[0] = gl == 0 ? myc : oc;        cK[1] = gl == 0 ? oc : myc;
       }
     }
+#ifdef PSB_ROUND_STATS
+    if (me && gl == 0 && a.mode == 1) atomicAdd(&a.counters[24 + rtype], 1ull);
+#endif
     if (me) {
       rounds++;
       int r = BIS_CONTINUE;
@@ -843,7 +864,7 @@ __global__ void __launch_bounds__(128) k_bisect(BisArgs a) {
         if (itp_round) {
           const bool caught = !(new_w > 2.5 * ifrac * old_w);
           use_itp = !(new_w > old_w / 3.0);
-          ifrac = caught ? fmax(ifrac * ifrac, 1e-7) : 0.0625;
+          ifrac = caught ? fmax(ifrac * sqrt(ifrac), 1e-7) : a.itp_frac0;
         } else {
           use_itp = true;
         }
