@@ -86,7 +86,7 @@ struct psb_handle {
   double k_cert_delta = 1e-16;  // PSB_CERT_DELTA=x (0: certificates off, the round-2 overflow rule alone)
   bool k_bexpand = true, k_fallback = true, k_seq = false;
   int k_bvariant = 0;
-  double k_lfrac = 1.0 / 3.0;
+  double k_lfrac = 0.0;  // 0: by the rule
   int k_defer = 16;
   int k_counts = 1;
   int k_lgmin = 256, k_lgratio = 20;
@@ -206,7 +206,7 @@ int psb_create(int device, psb_handle** out) {
   h->k_lgratio = getenv("PSB_LGRATIO") ? atoi(getenv("PSB_LGRATIO")) : 20;  // dev: ... and nA <= ratio * nB
   h->k_counts = getenv("PSB_COUNTS") ? atoi(getenv("PSB_COUNTS")) : 1;  // dev: 0 switches the count-guided probe placement off
   h->k_defer = getenv("PSB_DEFER") ? atoi(getenv("PSB_DEFER")) : 16;      // dev: engine-L step deferral (0: off)
-  h->k_lfrac = getenv("PSB_LFRAC") ? atof(getenv("PSB_LFRAC")) : 1.0 / 3.0;   // dev: SM share hosting an engine-L block (long general lists)
+  h->k_lfrac = getenv("PSB_LFRAC") ? atof(getenv("PSB_LFRAC")) : 0.0;   // dev: SM share hosting an engine-L block (long general lists)
   h->k_bfull = getenv("PSB_BFULL") ? atoi(getenv("PSB_BFULL")) : 1;     // dev: 0 restores the two-launch engine B on long general lists
   h->k_refill = getenv("PSB_REFILL") ? atoi(getenv("PSB_REFILL")) : 16;  // dev: engine-L refill threshold
   h->k_cert_delta = getenv("PSB_CERT_DELTA") ? atof(getenv("PSB_CERT_DELTA")) : 1e-16;
@@ -577,6 +577,9 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
   // 434/469/516/897/615, a third 428/462/509/891/614. Widening the rule from (1024 per SM, nA <= 3 nB) to
   // (256, 20) with the queued remainder: 20 of the 64 matrices 3..18% faster (matrix 1 147 -> 120 ms), one
   // slower (matrix 45, engine L as long as engine B: 162 -> 196 ms); C5 pass 13.77 -> 13.29 s.
+  // After the count-guided probe policy (engine B ~18% shorter) engine L outlasted engine B on 25 matrices,
+  // all with nA > 3 nB: two thirds of the SMs there (matrices 45/28/23/63/53/1: 192/237/276/123/156/114 ->
+  // 160/188/241/102/129/100 ms), a third where nA <= 3 nB (matrices 0/42 lose 3%/1% on two thirds).
   const bool long_general = bsw > 0 && nA > 0 && h->k_bfull && !h->k_seq &&
                             nB >= (int64_t)h->k_lgmin * h->num_sms && (int64_t)h->k_lgratio * nB >= nA;
   int64_t gridL = 0, gridL2 = 0;  // gridL2: engine L's second launch (long general lists), queued behind engine B
@@ -604,7 +607,9 @@ static int run_pipeline(psb_handle* h, const double2* d_zs, const int64_t* d_out
     warps = std::max<int64_t>(kLWarpsPerBlock, (warps + kLWarpsPerBlock - 1) / kLWarpsPerBlock * kLWarpsPerBlock);
     const int64_t warps_all = warps;  // every warp engine L may run (scratch is per warp)
     if (long_general) {
-      warps = std::min<int64_t>(warps, std::max<int64_t>(1, (int64_t)(h->k_lfrac * h->num_sms + 0.5)) * kLWarpsPerBlock);
+      // a third of the SMs where engine B is clearly the longer engine (nA <= 3 nB), two thirds otherwise
+      const double share = h->k_lfrac > 0 ? h->k_lfrac : (3 * nB >= nA ? 1.0 / 3.0 : 2.0 / 3.0);
+      warps = std::min<int64_t>(warps, std::max<int64_t>(1, (int64_t)(share * h->num_sms + 0.5)) * kLWarpsPerBlock);
       gridL2 = (warps_all - warps) / kLWarpsPerBlock;
     }
     gridL = warps / kLWarpsPerBlock;
