@@ -88,7 +88,7 @@ struct psb_handle {
   int k_bvariant = 0;
   double k_lfrac = 0.0;  // 0: by the rule
   int k_defer = 16;
-  int k_counts = 1;
+  int k_counts = 2;
   int k_lgmin = 256, k_lgratio = 20;
   int k_bfull = 1;
   struct FitEntry { const void* f; int lkey, btpb, tpb, occ, occFull; int64_t threads; int wregs; };
@@ -204,7 +204,7 @@ int psb_create(int device, psb_handle** out) {
   h->k_lwarps = getenv("PSB_LWARPS") ? atoll(getenv("PSB_LWARPS")) : 0;
   h->k_lgmin = getenv("PSB_LGMIN") ? atoi(getenv("PSB_LGMIN")) : 256;   // dev: long-general rule, min bisection points per SM
   h->k_lgratio = getenv("PSB_LGRATIO") ? atoi(getenv("PSB_LGRATIO")) : 20;  // dev: ... and nA <= ratio * nB
-  h->k_counts = getenv("PSB_COUNTS") ? atoi(getenv("PSB_COUNTS")) : 1;  // dev: 0 switches the count-guided probe placement off
+  h->k_counts = getenv("PSB_COUNTS") ? atoi(getenv("PSB_COUNTS")) : 2;  // dev: 0 count-guided probe placement off, 1 without the three-point chord
   h->k_defer = getenv("PSB_DEFER") ? atoi(getenv("PSB_DEFER")) : 16;      // dev: engine-L step deferral (0: off)
   h->k_lfrac = getenv("PSB_LFRAC") ? atof(getenv("PSB_LFRAC")) : 0.0;   // dev: SM share hosting an engine-L block (long general lists)
   h->k_bfull = getenv("PSB_BFULL") ? atoi(getenv("PSB_BFULL")) : 1;     // dev: 0 restores the two-launch engine B on long general lists
